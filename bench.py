@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""OSBF benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C1..C5] [--mode fast|exact] [--radius R]
+
+A *step* is one full pass of the hot path over one batch: ``iterations``
+Jacobi OSBF passes over the workload's planes (inputs resident in HBM).
+Default workload: BASELINE config C4 — 256 float32 images of 1024x1024, r=2,
+20 iterations — the largest batch-sharded config, the one the metric's
+"achieved HBM GB/s ... 1/2/4/8 B200" is meaningful for (C2's 100 MB working
+set sits in the 126 MB L2).  Multi-GPU: one process per GPU (torchrun), each
+rank filters its own full C4 batch (batch sharding, no data-path collective):
+``scaling = weak``.
+
+Rank 0 prints ONE JSON line.  Numbers: CUDA events on the launching stream,
+max over ranks; L2 flushed (256 MiB write) between timed steps and every
+buffer is larger than L2 anyway; nvidia-smi clocks sampled during the timed
+region.  ``e2e`` = same metric through the C ABI host entry point
+(osbf_gpu_osbf_host) with pinned host buffers, H2D + D2H inside the timing.
+``--impl reference`` times the reference's own CPU implementation (the
+unmodified reference headers compiled into oracle/_ref) on the box's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "OSBF megapixel-iterations/sec and achieved HBM GB/s vs peak, 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+IN_BYTES = {"u8": 1, "f32": 4, "f64": 8}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--mode", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--radius", type=int, default=None)
+    ap.add_argument("--iterations", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"osbf_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons, power = [], [], set(), []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                mask = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for bit, name in REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic(workload: str, mode: str, kernel: str):
+    """Per-launch dram bytes of the dominant kernel from the committed ncu
+    --set full summary (profiles/ncu_summary.json), if one exists."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[f"{workload}/{mode}/{kernel}"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def workload_desc(cfg, r, iters):
+    return (f"{cfg.name}: {cfg.batch} x {cfg.height}x{cfg.width} {cfg.dtype} seeded synthetic "
+            f"mosaic+noise, r={r}, {iters} iterations")
+
+
+def cpu_reference_rate(x, r, iters, budget_s: float, threads: int):
+    """Time the reference CPU path (oracle/_ref, else the oracle port) on a
+    bounded prefix of the batch; returns (Mpx-iter/s, kind, sample)."""
+    import numpy as np
+
+    import oracle
+
+    if oracle.Reference.available():
+        ref = oracle.Reference()
+        ref.pin_allocator_for_timing()
+        ref.set_max_threads(threads)
+        run = lambda p: ref.osbf(p, r, iters)  # noqa: E731
+        kind = "reference"
+    else:
+        orc = oracle.Oracle()
+        run = lambda p: orc.osbf(p, r, iters, threads=threads)  # noqa: E731
+        kind = "port"
+    planes = x.reshape(-1, x.shape[-2], x.shape[-1])
+    # vCPU warm-up (the first multi-threaded run after idle is slow)
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        run(np.asarray(planes[0][:256, :256], dtype=np.float64))
+    t0 = time.perf_counter()
+    run(np.asarray(planes[0], dtype=np.float64))
+    t1 = time.perf_counter() - t0
+    n = int(max(1, min(len(planes), budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    for i in range(n):
+        run(np.asarray(planes[i], dtype=np.float64))
+    dt = time.perf_counter() - t0
+    px = n * planes.shape[1] * planes.shape[2] * iters
+    sample = (f"{n} of {len(planes)} planes x {iters} iterations ({px / 1e6:.1f} Mpx-iter, "
+              f"{dt:.1f} s), reference osbf::osbf in double")
+    return px / dt / 1e6, kind, sample
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2108_05021_b200 import synth
+
+    cfg = synth.CONFIGS[args.workload]
+    r = args.radius or cfg.radius
+    iters = args.iterations or cfg.iterations
+    import numpy as np
+
+    import oracle
+
+    x = synth.make_input(args.workload)
+    planes = x.reshape(-1, x.shape[-2], x.shape[-1])
+    threads = os.cpu_count() or 1
+    if oracle.Reference.available():
+        ref = oracle.Reference()
+        ref.pin_allocator_for_timing()
+        ref.set_max_threads(threads)
+        run = lambda p, it: ref.osbf(p, r, it)  # noqa: E731
+        kind = "reference"
+    else:
+        orc = oracle.Oracle()
+        run = lambda p, it: orc.osbf(p, r, it, threads=threads)  # noqa: E731
+        kind = "port"
+    # bounded sample per step: one plane, as many iterations as fit ~1.5 s
+    p0 = np.asarray(planes[0], dtype=np.float64)
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        run(p0[:256, :256], 1)
+    t0 = time.perf_counter()
+    run(p0, 1)
+    t_it = time.perf_counter() - t0
+    it_per_step = int(max(1, min(iters, 1.5 / max(t_it, 1e-6))))
+    px_step = p0.size * it_per_step
+    for i in range(args.warmup):
+        run(np.asarray(planes[i % len(planes)], dtype=np.float64), it_per_step)
+    times = []
+    for i in range(args.steps):
+        p = np.asarray(planes[i % len(planes)], dtype=np.float64)
+        t0 = time.perf_counter()
+        run(p, it_per_step)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = px_step * args.steps / total / 1e6
+    sample = (f"per step: 1 plane of {p0.shape[0]}x{p0.shape[1]} x {it_per_step} of {iters} "
+              f"iterations (per-iteration cost is constant), {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpx-iter/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, r, iters), "radius": r, "iterations": iters,
+                   "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpx-iter/s", "cores": threads,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mpx-iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2108_05021_b200 as ob
+    from paper_2108_05021_b200 import synth
+
+    torch.cuda.set_device(local)
+    cfg = synth.CONFIGS[args.workload]
+    r = args.radius or cfg.radius
+    iters = args.iterations or cfg.iterations
+    x = synth.make_input(args.workload)  # (B, H, W), seeded, identical on every rank
+    B, H, W = x.shape
+    px = B * H * W
+    ctx = ob.Context(local)
+    d_in = torch.from_numpy(x).cuda()
+    d_out = torch.empty((B, H, W), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 0)):
+        ctx.iterate(d_in, r, iters, mode=args.mode, out=d_out)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    launches0 = ctx.launches
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)  # evict L2 between timed steps (not timed)
+        starts[i].record(stream)
+        ctx.iterate(d_in, r, iters, mode=args.mode, out=d_out)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = allreduce_max(sum(step_ms), world)
+    launches_all = int(allreduce_sum(launches, world))
+    value = world * px * iters * args.steps / (total_ms / 1000.0) / 1e6
+
+    # Roofline of the dominant kernel.  Fast mode: every launch of the step is
+    # fast_tile_step, back to back on this stream, so its average launch
+    # duration is the step time / iterations.  Algorithmic bytes per
+    # pixel-iteration: read U^t once + write U^{t+1} once (fp64 storage; the
+    # first pass reads the input dtype).
+    in_b = IN_BYTES[cfg.dtype]
+    alg_bytes_step = px * ((in_b + 8) + (iters - 1) * 16)
+    per_launch_bytes = alg_bytes_step / iters
+    if args.mode == "fast":
+        kernel = "fast_tile_step"
+        kernel_ms = sum(step_ms) / (args.steps * iters)
+        launches_per_pass = 1
+    else:
+        kernel = "exact pass (row_prefix + col_chain + stencil)"
+        kernel_ms = sum(step_ms) / (args.steps * iters)
+        launches_per_pass = 3
+    achieved = per_launch_bytes / (kernel_ms / 1000.0) / 1e9
+    peak, peak_kind = hbm_peak()
+    traffic = ncu_traffic(args.workload, args.mode, kernel.split()[0])
+
+    result = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mpx-iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, r, iters), "batch_per_gpu": B, "height": H,
+                   "width": W, "radius": r, "iterations": iters, "mode": args.mode,
+                   "storage": "f64 between passes (input dtype on the first pass)",
+                   "l2": "L2 flushed (256 MiB write) between timed steps",
+                   "parallelism": f"batch-sharded dp{world} (each rank its own {B}-plane batch)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "kernel": kernel,
+                     "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                     "avg_launch_ms": round(kernel_ms, 5),
+                     "bytes_rule": "per pixel-iteration: read U^t + write U^{t+1} "
+                                   f"(first pass {in_b}+8 B, then 8+8 B)"},
+        "gpu_launches": launches_all,
+        "launches_per_pass": launches_per_pass,
+        "clocks": clk,
+    }
+
+    if not args.no_e2e:
+        # End to end through the C ABI host entry point: pinned host input
+        # (float32, as generated) -> H2D -> iterations -> D2H (f64) -> host.
+        h_in = torch.from_numpy(x).pin_memory()
+        h_out = torch.empty((B, H, W), dtype=torch.float64).pin_memory()
+        lib = ctx._lib
+        import ctypes
+
+        code = {"u8": 0, "f32": 1, "f64": 2}[cfg.dtype]
+        mcode = {"exact": 0, "fast": 1}[args.mode]
+
+        def e2e_call():
+            st = lib.osbf_gpu_osbf_host(ctx.handle, code, ctypes.c_void_p(h_in.data_ptr()),
+                                        ctypes.c_void_p(h_out.data_ptr()), W, H, B, r, iters, mcode)
+            if st != 0:
+                raise RuntimeError(lib.osbf_gpu_last_error().decode())
+
+        e2e_call()
+        e2e_steps = max(1, min(args.steps, 5))
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_call()
+        dt = allreduce_max(time.perf_counter() - t0, world)
+        result["e2e"] = {"value": round(world * px * iters * e2e_steps / dt / 1e6, 3),
+                         "unit": "Mpx-iter/s", "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()),
+                         "d2h_bytes_per_step": int(h_out.numel() * 8), "steps": e2e_steps,
+                         "api": "osbf_gpu_osbf_host (C ABI, pinned host buffers)"}
+        # sanity: the e2e output equals the device path's output bit for bit
+        result["e2e"]["matches_device_path"] = bool(
+            torch.equal(h_out.view(torch.int64), d_out.cpu().view(torch.int64)))
+
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        v, kind, sample = cpu_reference_rate(x, r, iters, budget_s=15.0,
+                                             threads=os.cpu_count() or 1)
+        result["cpu_baseline"] = {"value": round(v, 3), "unit": "Mpx-iter/s",
+                                  "cores": os.cpu_count() or 1, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

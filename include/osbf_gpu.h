@@ -1,0 +1,154 @@
+/*
+ * osbf_gpu.h — C ABI of the B200-native One-Sided Box Filter (OSBF) library
+ * (libosbf_gpu.so, hand-written sm_100a CUDA).
+ *
+ * This is the drop-in boundary for the reference's exact-OSBF hot path.  The
+ * reference is header-only C++ (namespace osbf, /root/reference/proj/include);
+ * the C++ headers in include/osbf/ keep its declarations and forward to the
+ * entry points below.  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj/include/osbf/).
+ *
+ * Conventions
+ *  - Planes are row-major, x (column) fastest: sample(x,y) = base[y*pitch + x]
+ *    (core.hpp:61-63).  `pitch` is in ELEMENTS of the plane's dtype.
+ *  - A batch is `batch` planes of identical size, `plane_stride` elements apart
+ *    (channels of a MultiChannelImage are batch entries).
+ *  - Outputs are always fp64, like ImagePlane (core.hpp:73).
+ *  - Every function returns an osbf_status; on failure osbf_gpu_last_error()
+ *    returns a thread-local message.  Status codes map 1:1 onto the exception
+ *    types the reference throws (std::invalid_argument, std::domain_error,
+ *    std::out_of_range); CUDA failures are OSBF_ERR_CUDA.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with OSBF_ERR_NO_DEVICE.
+ */
+#ifndef OSBF_GPU_H
+#define OSBF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSBF_GPU_ABI_VERSION 1
+
+typedef enum osbf_status {
+    OSBF_OK = 0,
+    OSBF_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    OSBF_ERR_DOMAIN = 2,           /* reference: std::domain_error     */
+    OSBF_ERR_OUT_OF_RANGE = 3,     /* reference: std::out_of_range     */
+    OSBF_ERR_CUDA = 4,             /* CUDA runtime / launch failure     */
+    OSBF_ERR_NO_DEVICE = 5,        /* no usable sm_100 GPU              */
+    OSBF_ERR_ALLOC = 6             /* device or pinned allocation failed */
+} osbf_status;
+
+typedef enum osbf_dtype {
+    OSBF_U8 = 0,  /* 8-bit integer samples, promoted exactly to fp64 */
+    OSBF_F32 = 1, /* float32 samples, promoted exactly to fp64       */
+    OSBF_F64 = 2  /* fp64 samples (the reference's ImagePlane)        */
+} osbf_dtype;
+
+typedef enum osbf_mode {
+    /* Bit-identical to the reference: replays the whole-image fp64
+     * summed-area table in the reference's serial order (integral.hpp:16-30),
+     * ((A-B)-C)+D window sums (integral.hpp:48-49), IEEE division by the
+     * valid count (integral.hpp:68) and the strict-< first-minimum selection
+     * (filters2d.hpp:72-82).  Default for the drop-in C++ API. */
+    OSBF_MODE_EXACT = 0,
+    /* Tile-local fp64 sums (no whole-image prefix, no drift on huge images),
+     * same selection rule.  Bit-identical to the reference whenever the
+     * window sums are exact (integer-valued input, e.g. uint8 first pass);
+     * otherwise within a few fp64 ulps per pass. */
+    OSBF_MODE_FAST = 1
+} osbf_mode;
+
+typedef struct osbf_ctx osbf_ctx;
+
+/* ---- library / context --------------------------------------------------- */
+
+int osbf_gpu_abi_version(void);
+/* Thread-local text of the last failure on this thread ("" if none). */
+const char* osbf_gpu_last_error(void);
+/* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
+int osbf_gpu_device_available(void);
+
+/* A context owns device scratch (ping-pong planes, SAT workspace) and a
+ * default stream on `device`.  Reentrant per context; use one per thread. */
+osbf_status osbf_gpu_ctx_create(int device, osbf_ctx** out);
+osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx);
+/* Release cached scratch (it is regrown on demand). */
+osbf_status osbf_gpu_ctx_trim(osbf_ctx* ctx);
+/* Number of kernels this context has launched so far (instrumentation). */
+uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx);
+
+/* ---- device-resident entry points (throughput path) ---------------------- */
+
+/*
+ * Replaces osbf::osbf (filters2d.hpp:91-98) and, for iterations == 1,
+ * osbf::osbf_step (filters2d.hpp:61-88), batched over `batch` planes.
+ *   d_in  : device pointer, dtype `in_dtype`, batch x height x in_pitch
+ *   d_out : device pointer, fp64, batch x height x out_pitch (may alias d_in
+ *           only when in_dtype == OSBF_F64 and the pitches/strides match)
+ *   stream: cudaStream_t (NULL = the context's stream); the call is
+ *           asynchronous with respect to the host.
+ * Errors (reference behaviour): iterations < 0 -> INVALID_ARGUMENT
+ * (filters2d.hpp:92-93); radius < 1 with iterations > 0 -> INVALID_ARGUMENT
+ * (filters2d.hpp:62-63); iterations == 0 copies without checking radius
+ * (filters2d.hpp:94-97); width or height < 1 -> INVALID_ARGUMENT (core.hpp:20-21).
+ */
+osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                             size_t in_pitch, size_t in_plane_stride, double* d_out,
+                             size_t out_pitch, size_t out_plane_stride, int width, int height,
+                             int batch, int radius, int iterations, osbf_mode mode,
+                             void* stream);
+
+/*
+ * Per-pixel diagnostics for one pass over `batch` planes (exact SAT):
+ *   d_means (nullable): fp64 [batch][height][width][8] — subwindow_means
+ *                       (filters2d.hpp:26-34) at every pixel;
+ *   d_sel   (nullable): uint8 [batch][height][width] — 1-based id of the
+ *                       window osbf_step selects (filters2d.hpp:72-82).
+ */
+osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                                     size_t in_pitch, size_t in_plane_stride, int width,
+                                     int height, int batch, int radius, double* d_means,
+                                     uint8_t* d_sel, osbf_mode mode, void* stream);
+
+/*
+ * Whole-image summed-area table, bit-identical to SummedAreaTable
+ * (integral.hpp:16-30): d_cumsum is fp64 [batch][height+1][width+1].
+ */
+osbf_status osbf_gpu_sat(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in, size_t in_pitch,
+                         size_t in_plane_stride, int width, int height, int batch,
+                         double* d_cumsum, void* stream);
+
+/* ---- host-buffer entry points (what the drop-in C++ API calls) ------------ */
+
+/* osbf::osbf on host memory: copies in, filters, copies out, synchronizes.
+ * h_in has `batch` planes of width*height samples back to back (dtype
+ * in_dtype); h_out receives batch*width*height doubles. */
+osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                               double* h_out, int width, int height, int batch, int radius,
+                               int iterations, osbf_mode mode);
+
+/* osbf::osbf_step (filters2d.hpp:61-88) on one host plane: always validates r. */
+osbf_status osbf_gpu_osbf_step_host(osbf_ctx* ctx, const double* h_in, double* h_out, int width,
+                                    int height, int radius, osbf_mode mode);
+
+/* osbf::filter_multichannel, OsbfExact branch (filters2d.hpp:371-400):
+ * `channels` (1..4) separate host planes, each width*height doubles. */
+osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const* h_in,
+                                              double* const* h_out, int channels, int width,
+                                              int height, int radius, int iterations,
+                                              osbf_mode mode);
+
+/* SummedAreaTable construction (integral.hpp:16-30) for host planes. */
+osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,
+                              double* h_cumsum);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSBF_GPU_H */

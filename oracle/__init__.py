@@ -1,0 +1,202 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the CPU parity checkers.
+
+* ``Oracle`` wraps ``oracle/liboracle.so`` — the plain-C restatement of the
+  reference OSBF path (``osbf_oracle.c``; every function cites the reference
+  file:line it follows).
+* ``Reference`` wraps ``oracle/_ref/libosbf_ref.so`` — the unmodified
+  reference headers (``/root/reference/proj/include``) compiled behind a C
+  shim (``ref_shim.cpp``).  It is built here and travels to the GPU box as a
+  prebuilt file; nothing reads ``/root/reference`` at run time.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and the CPU-baseline legs of
+``bench.py`` may import this package.  The product path never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libosbf_ref.so")
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+def build() -> None:
+    """Compile liboracle.so (+ _ref when the reference tree is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a: np.ndarray, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+def _as_f64(plane) -> np.ndarray:
+    return np.ascontiguousarray(plane, dtype=np.float64)
+
+
+class CheckerError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: status {status}")
+        self.status = status
+
+
+class Oracle:
+    """The C restatement (osbf_oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build()
+        lib = ctypes.CDLL(path)
+        lib.oracle_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.oracle_osbf_mt.argtypes = lib.oracle_osbf.argtypes + [ctypes.c_int]
+        lib.oracle_osbf_step.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _u8p]
+        lib.oracle_sat_build.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
+        lib.oracle_sat_build.restype = None
+        lib.oracle_rect_sum.argtypes = [_dp] + [ctypes.c_int] * 6
+        lib.oracle_rect_sum.restype = ctypes.c_double
+        lib.oracle_rect_count.argtypes = [ctypes.c_int] * 6
+        lib.oracle_rect_count.restype = ctypes.c_longlong
+        lib.oracle_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
+        lib.oracle_subwindow_means.argtypes = [_dp] + [ctypes.c_int] * 5 + [_dp]
+        lib.oracle_sub_windows.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        self.lib = lib
+
+    def sub_windows(self, r: int):
+        buf = (ctypes.c_int * 40)()
+        st = self.lib.oracle_sub_windows(r, buf)
+        if st:
+            raise CheckerError(st, "sub_windows")
+        return [tuple(buf[i * 5:(i + 1) * 5]) for i in range(8)]
+
+    def osbf(self, plane, r: int, iterations: int, threads: int = 1) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.oracle_osbf_mt(_ptr(p), _ptr(out), w, h, r, iterations, threads)
+        if st:
+            raise CheckerError(st, "osbf")
+        return out
+
+    def osbf_step(self, plane, r: int, with_selection: bool = False):
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        sel = np.zeros((h, w), dtype=np.uint8)
+        st = self.lib.oracle_osbf_step(_ptr(p), _ptr(out), w, h, r, _ptr(sel, _u8p))
+        if st:
+            raise CheckerError(st, "osbf_step")
+        return (out, sel) if with_selection else out
+
+    def sat(self, plane) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        c = np.empty((h + 1, w + 1), dtype=np.float64)
+        self.lib.oracle_sat_build(_ptr(p), w, h, _ptr(c))
+        return c
+
+    def subwindow_means(self, cumsum: np.ndarray, w: int, h: int, x: int, y: int, r: int):
+        out = np.empty(8, dtype=np.float64)
+        st = self.lib.oracle_subwindow_means(_ptr(cumsum), w, h, x, y, r, _ptr(out))
+        if st:
+            raise CheckerError(st, "subwindow_means")
+        return out
+
+    def rect_mean(self, cumsum, w, h, x0, y0, x1, y1) -> float:
+        m = ctypes.c_double()
+        st = self.lib.oracle_rect_mean(_ptr(cumsum), w, h, x0, y0, x1, y1, ctypes.byref(m))
+        if st:
+            raise CheckerError(st, "rect_mean")
+        return m.value
+
+
+class Reference:
+    """The unmodified reference headers behind ref_shim.cpp (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        lib = ctypes.CDLL(path)
+        lib.ref_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.ref_osbf_step.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.ref_filter_multichannel.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
+        lib.ref_sat.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
+        lib.ref_subwindow_means.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _u8p]
+        lib.ref_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
+        lib.ref_set_max_threads.argtypes = [ctypes.c_int]
+        lib.ref_set_max_threads.restype = None
+        lib.ref_pin_allocator_for_timing.restype = None
+        self.lib = lib
+
+    @staticmethod
+    def available(path: str = REF_SO) -> bool:
+        return os.path.exists(path)
+
+    def set_max_threads(self, n: int) -> None:
+        self.lib.ref_set_max_threads(n)
+
+    def max_threads(self) -> int:
+        return self.lib.ref_max_threads()
+
+    def pin_allocator_for_timing(self) -> None:
+        self.lib.ref_pin_allocator_for_timing()
+
+    def osbf(self, plane, r: int, iterations: int) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.ref_osbf(_ptr(p), _ptr(out), w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "ref osbf")
+        return out
+
+    def osbf_step(self, plane, r: int) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.ref_osbf_step(_ptr(p), _ptr(out), w, h, r)
+        if st:
+            raise CheckerError(st, "ref osbf_step")
+        return out
+
+    def filter_multichannel(self, planes, r: int, iterations: int) -> np.ndarray:
+        p = _as_f64(planes)
+        c, h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.ref_filter_multichannel(_ptr(p), _ptr(out), c, w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "ref filter_multichannel")
+        return out
+
+    def sat(self, plane) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        c = np.empty((h + 1, w + 1), dtype=np.float64)
+        st = self.lib.ref_sat(_ptr(p), w, h, _ptr(c))
+        if st:
+            raise CheckerError(st, "ref sat")
+        return c
+
+    def subwindow_means(self, plane, r: int):
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty((h, w, 8), dtype=np.float64)
+        sel = np.zeros((h, w), dtype=np.uint8)
+        st = self.lib.ref_subwindow_means(_ptr(p), w, h, r, _ptr(out), _ptr(sel, _u8p))
+        if st:
+            raise CheckerError(st, "ref subwindow_means")
+        return out, sel
+
+    def rect_mean(self, plane, x0, y0, x1, y1) -> float:
+        p = _as_f64(plane)
+        h, w = p.shape
+        m = ctypes.c_double()
+        st = self.lib.ref_rect_mean(_ptr(p), w, h, x0, y0, x1, y1, ctypes.byref(m))
+        if st:
+            raise CheckerError(st, "ref rect_mean")
+        return m.value

@@ -1,0 +1,202 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — CPU restatement of the reference OSBF path.
+ * See osbf_oracle.h.  Reference citations are relative to
+ * /root/reference/proj/include/osbf/.
+ *
+ * Build: oracle/Makefile (gcc -O2 -std=c11, no -ffast-math; x86-64 baseline
+ * has no FMA so nothing can be contracted and the op order is the source
+ * order, exactly like the reference built with its CMake Release flags).
+ */
+#include "osbf_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+int oracle_sub_windows(int r, int out[8][5]) {
+    /* core.hpp:212-225 — order is the tie-break order (first minimum wins). */
+    if (r < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    const int t[8][5] = {
+        {1, -r, 0, 0, r}, {2, 0, r, 0, r},  {3, 0, r, -r, 0}, {4, -r, 0, -r, 0},
+        {5, -r, 0, -r, r}, {6, 0, r, -r, r}, {7, -r, r, 0, r}, {8, -r, r, -r, 0},
+    };
+    memcpy(out, t, sizeof(t));
+    return ORACLE_OK;
+}
+
+void oracle_sat_build(const double* plane, int w, int h, double* cumsum) {
+    /* integral.hpp:16-30: serial row running sum, then add the table row above. */
+    const size_t stride = (size_t)w + 1;
+    memset(cumsum, 0, sizeof(double) * stride * ((size_t)h + 1));
+    for (int y = 0; y < h; ++y) {
+        double row = 0.0;
+        const double* src = plane + (size_t)y * w;
+        const double* above = cumsum + (size_t)y * stride;
+        double* out = cumsum + (size_t)(y + 1) * stride;
+        for (int x = 0; x < w; ++x) {
+            row += src[x];
+            out[x + 1] = above[x + 1] + row;
+        }
+    }
+}
+
+static inline int imax(int a, int b) { return a > b ? a : b; }
+static inline int imin(int a, int b) { return a < b ? a : b; }
+
+double oracle_rect_sum(const double* c, int w, int h, int x0, int y0, int x1, int y1) {
+    /* integral.hpp:41-50 */
+    x0 = imax(x0, 0);
+    y0 = imax(y0, 0);
+    x1 = imin(x1, w - 1);
+    y1 = imin(y1, h - 1);
+    if (x0 > x1 || y0 > y1) return 0.0;
+    const size_t s = (size_t)w + 1;
+    return c[(size_t)(y1 + 1) * s + (x1 + 1)] - c[(size_t)(y1 + 1) * s + x0] -
+           c[(size_t)y0 * s + (x1 + 1)] + c[(size_t)y0 * s + x0];
+}
+
+long long oracle_rect_count(int w, int h, int x0, int y0, int x1, int y1) {
+    /* integral.hpp:53-61 */
+    x0 = imax(x0, 0);
+    y0 = imax(y0, 0);
+    x1 = imin(x1, w - 1);
+    y1 = imin(y1, h - 1);
+    if (x0 > x1 || y0 > y1) return 0;
+    return (long long)(x1 - x0 + 1) * (y1 - y0 + 1);
+}
+
+int oracle_rect_mean(const double* c, int w, int h, int x0, int y0, int x1, int y1,
+                     double* mean) {
+    /* integral.hpp:64-69 */
+    const long long n = oracle_rect_count(w, h, x0, y0, x1, y1);
+    if (n == 0) return ORACLE_ERR_DOMAIN;
+    *mean = oracle_rect_sum(c, w, h, x0, y0, x1, y1) / (double)n;
+    return ORACLE_OK;
+}
+
+int oracle_subwindow_means(const double* c, int w, int h, int x, int y, int r, double out[8]) {
+    /* filters2d.hpp:26-34 */
+    int wins[8][5];
+    int st = oracle_sub_windows(r, wins);
+    if (st) return st;
+    for (int i = 0; i < 8; ++i) {
+        st = oracle_rect_mean(c, w, h, x + wins[i][1], y + wins[i][3], x + wins[i][2],
+                              y + wins[i][4], &out[i]);
+        if (st) return st;
+    }
+    return ORACLE_OK;
+}
+
+/* Inner loop of filters2d.hpp:68-86 over rows [y0, y1). */
+static void step_rows(const double* in, const double* c, double* out, uint8_t* sel, int w,
+                      int h, int wins[8][5], int y0, int y1) {
+    for (int y = y0; y < y1; ++y) {
+        for (int x = 0; x < w; ++x) {
+            const double u = in[(size_t)y * w + x];
+            double best = 0.0;
+            double best_abs = INFINITY;
+            int best_id = 0;
+            for (int i = 0; i < 8; ++i) {
+                double a;
+                /* every window contains (x,y) so the mean never throws */
+                oracle_rect_mean(c, w, h, x + wins[i][1], y + wins[i][3], x + wins[i][2],
+                                 y + wins[i][4], &a);
+                const double d = fabs(a - u);
+                if (d < best_abs) {
+                    best_abs = d;
+                    best = a;
+                    best_id = i + 1;
+                }
+            }
+            out[(size_t)y * w + x] = best;
+            if (sel) sel[(size_t)y * w + x] = (uint8_t)best_id;
+        }
+    }
+}
+
+int oracle_osbf_step(const double* in, double* out, int w, int h, int r, uint8_t* sel) {
+    /* filters2d.hpp:61-88 */
+    int wins[8][5];
+    if (oracle_sub_windows(r, wins)) return ORACLE_ERR_INVALID_ARGUMENT;
+    if (w < 1 || h < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    double* c = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1));
+    if (!c) return ORACLE_ERR_INVALID_ARGUMENT;
+    oracle_sat_build(in, w, h, c);
+    step_rows(in, c, out, sel, w, h, wins, 0, h);
+    free(c);
+    return ORACLE_OK;
+}
+
+typedef struct {
+    const double* in;
+    const double* c;
+    double* out;
+    int w, h, y0, y1;
+    int (*wins)[5];
+} rows_job;
+
+static void* rows_worker(void* p) {
+    rows_job* j = (rows_job*)p;
+    step_rows(j->in, j->c, j->out, NULL, j->w, j->h, j->wins, j->y0, j->y1);
+    return NULL;
+}
+
+static int osbf_impl(const double* in, double* out, int w, int h, int r, int iterations,
+                     int threads) {
+    /* filters2d.hpp:91-98 — iterations==0 is a copy and does not validate r. */
+    if (iterations < 0) return ORACLE_ERR_INVALID_ARGUMENT;
+    if (w < 1 || h < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h;
+    if (iterations == 0) {
+        memmove(out, in, sizeof(double) * n);
+        return ORACLE_OK;
+    }
+    int wins[8][5];
+    if (oracle_sub_windows(r, wins)) return ORACLE_ERR_INVALID_ARGUMENT;
+    double* cur = (double*)malloc(sizeof(double) * n);
+    double* nxt = (double*)malloc(sizeof(double) * n);
+    double* c = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1));
+    if (!cur || !nxt || !c) {
+        free(cur); free(nxt); free(c);
+        return ORACLE_ERR_INVALID_ARGUMENT;
+    }
+    memcpy(cur, in, sizeof(double) * n);
+    if (threads < 1) threads = 1;
+    if (threads > h) threads = h;
+    pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    rows_job* jobs = (rows_job*)malloc(sizeof(rows_job) * (size_t)threads);
+    for (int it = 0; it < iterations; ++it) {
+        oracle_sat_build(cur, w, h, c);
+        if (threads == 1) {
+            step_rows(cur, c, nxt, NULL, w, h, wins, 0, h);
+        } else {
+            const int chunk = (h + threads - 1) / threads;
+            int started = 0;
+            for (int t = 0; t < threads; ++t) {
+                const int y0 = t * chunk, y1 = imin(h, y0 + chunk);
+                if (y0 >= y1) break;
+                jobs[t] = (rows_job){cur, c, nxt, w, h, y0, y1, wins};
+                pthread_create(&tids[t], NULL, rows_worker, &jobs[t]);
+                ++started;
+            }
+            for (int t = 0; t < started; ++t) pthread_join(tids[t], NULL);
+        }
+        double* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+    memcpy(out, cur, sizeof(double) * n);
+    free(tids); free(jobs);
+    free(cur); free(nxt); free(c);
+    return ORACLE_OK;
+}
+
+int oracle_osbf(const double* in, double* out, int w, int h, int r, int iterations) {
+    return osbf_impl(in, out, w, h, r, iterations, 1);
+}
+
+int oracle_osbf_mt(const double* in, double* out, int w, int h, int r, int iterations,
+                   int threads) {
+    return osbf_impl(in, out, w, h, r, iterations, threads);
+}

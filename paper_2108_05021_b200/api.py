@@ -1,0 +1,386 @@
+"""Python mirror of the reference's exact-OSBF interface, over libosbf_gpu.so.
+
+The reference API (namespace ``osbf``, /root/reference/proj/include/osbf/) is
+C++; the drop-in C++ headers live in ``include/osbf/``.  This module exposes
+the same operations to Python with the same names, argument meaning and
+error behaviour, for tests, the benchmark and Python callers:
+
+=====================================  =============================================
+reference                              here
+=====================================  =============================================
+``sub_windows(r)`` core.hpp:212        :func:`sub_windows`
+``FilterVariant`` / ``FilterConfig``   :class:`FilterVariant` / :class:`FilterConfig`
+ core.hpp:227-254
+``build_sat`` integral.hpp:77          :func:`build_sat` (GPU, bit-identical table)
+``subwindow_means`` filters2d.hpp:26   :func:`subwindow_means` (all pixels at once)
+``osbf_step`` filters2d.hpp:61         :func:`osbf_step`
+``osbf`` filters2d.hpp:91              :func:`osbf`
+``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact only)
+``set_max_threads`` parallel.hpp:20    :func:`set_max_threads` (no-op: the GPU
+                                        result does not depend on any launch knob)
+=====================================  =============================================
+
+Inputs may be numpy arrays (host path: the C ABI copies in and out) or
+CUDA torch tensors (device path: no host round trip, caller's stream).
+Exceptions: ``InvalidArgument`` (std::invalid_argument), ``DomainError``
+(std::domain_error), ``OutOfRange`` (std::out_of_range), ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+class OsbfError(RuntimeError):
+    """Base class; ``status`` is the osbf_status code."""
+
+    status = -1
+
+
+class InvalidArgument(OsbfError, ValueError):
+    status = N.OSBF_ERR_INVALID_ARGUMENT
+
+
+class DomainError(OsbfError, ArithmeticError):
+    status = N.OSBF_ERR_DOMAIN
+
+
+class OutOfRange(OsbfError, IndexError):
+    status = N.OSBF_ERR_OUT_OF_RANGE
+
+
+class CudaError(OsbfError):
+    status = N.OSBF_ERR_CUDA
+
+
+class NoDevice(OsbfError):
+    status = N.OSBF_ERR_NO_DEVICE
+
+
+class AllocError(CudaError):
+    status = N.OSBF_ERR_ALLOC
+
+
+_ERRORS = {c.status: c for c in (InvalidArgument, DomainError, OutOfRange, CudaError, NoDevice,
+                                 AllocError)}
+
+
+def _check(st: int) -> None:
+    if st != N.OSBF_OK:
+        msg = N.lib().osbf_gpu_last_error().decode(errors="replace")
+        raise _ERRORS.get(st, OsbfError)(msg)
+
+
+def _mode_code(mode) -> int:
+    if isinstance(mode, int):
+        return mode
+    try:
+        return N.MODES[mode]
+    except KeyError:
+        raise InvalidArgument(f"unknown mode {mode!r}") from None
+
+
+# ---------------------------------------------------------------------------
+# reference value types (core.hpp)
+
+
+@dataclass(frozen=True)
+class SubWindowId:
+    """One-sided sub-window, core.hpp:201-205: u = column offsets, v = row offsets."""
+
+    id: int
+    u0: int
+    u1: int
+    v0: int
+    v1: int
+
+
+def sub_windows(r: int) -> list[SubWindowId]:
+    """The eight windows in selection (tie-break) order, core.hpp:212-225."""
+    if r < 1:
+        raise InvalidArgument("sub_windows: radius must be >= 1")
+    return [SubWindowId(1, -r, 0, 0, r), SubWindowId(2, 0, r, 0, r), SubWindowId(3, 0, r, -r, 0),
+            SubWindowId(4, -r, 0, -r, 0), SubWindowId(5, -r, 0, -r, r), SubWindowId(6, 0, r, -r, r),
+            SubWindowId(7, -r, r, 0, r), SubWindowId(8, -r, r, -r, 0)]
+
+
+class FilterVariant(enum.Enum):
+    """core.hpp:227-233.  Only OsbfExact is on this library's path."""
+
+    Box = 0
+    OsbfExact = 1
+    OsbfFast = 2
+    OneSidedGeneric = 3
+    Gaussian = 4
+
+
+@dataclass
+class FilterConfig:
+    """core.hpp:238-254 (defaults r=2, iterations=10, OsbfExact, sigma=3)."""
+
+    radius: int = 2
+    iterations: int = 10
+    variant: FilterVariant = FilterVariant.OsbfExact
+    sigma: float = 3.0
+
+    def validate(self) -> None:
+        if self.radius < 1:
+            raise InvalidArgument("FilterConfig: radius must be >= 1")
+        if self.iterations < 0:
+            raise InvalidArgument("FilterConfig: iterations must be >= 0")
+        if self.variant in (FilterVariant.OneSidedGeneric, FilterVariant.Gaussian) and \
+                not self.sigma > 0.0:
+            raise InvalidArgument("FilterConfig: sigma must be > 0")
+
+
+def set_max_threads(n: int) -> None:
+    """parallel.hpp:20 — accepted for API compatibility; GPU results are
+    identical for any launch configuration, so there is nothing to cap."""
+
+
+def max_threads() -> int:
+    return 1
+
+
+# ---------------------------------------------------------------------------
+# contexts
+
+
+class Context:
+    """Owns an ``osbf_ctx`` (device scratch + stream) on one GPU."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.lib()
+        h = ctypes.c_void_p()
+        _check(self._lib.osbf_gpu_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.osbf_gpu_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.osbf_gpu_ctx_launch_count(self.handle))
+
+    # -- device tensors -----------------------------------------------------
+    def iterate(self, src, radius: int, iterations: int, mode="exact", out=None, stream=None):
+        """osbf over a CUDA tensor of shape (H, W) or (B, H, W), dtype uint8 /
+        float32 / float64.  Returns (or fills) a float64 tensor of that shape."""
+        import torch
+
+        x, batch, h, w = _as_batch(src)
+        if out is None:
+            out = torch.empty((batch, h, w), dtype=torch.float64, device=x.device)
+            ret = out.view(src.shape)
+        else:
+            ret = out
+            out = out.view(batch, h, w)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        _check(self._lib.osbf_gpu_iterate(
+            self.handle, _dtype_code(x), ctypes.c_void_p(x.data_ptr()), x.stride(1), x.stride(0),
+            ctypes.c_void_p(out.data_ptr()), out.stride(1), out.stride(0), w, h, batch, radius,
+            iterations, _mode_code(mode), ctypes.c_void_p(stream)))
+        return ret
+
+    def subwindow_means(self, src, radius: int, mode="exact", stream=None):
+        """All-pixel subwindow_means (filters2d.hpp:26-34) and the selection map."""
+        import torch
+
+        x, batch, h, w = _as_batch(src)
+        means = torch.empty((batch, h, w, 8), dtype=torch.float64, device=x.device)
+        sel = torch.empty((batch, h, w), dtype=torch.uint8, device=x.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        _check(self._lib.osbf_gpu_subwindow_means(
+            self.handle, _dtype_code(x), ctypes.c_void_p(x.data_ptr()), x.stride(1), x.stride(0),
+            w, h, batch, radius, ctypes.c_void_p(means.data_ptr()), ctypes.c_void_p(sel.data_ptr()),
+            _mode_code(mode), ctypes.c_void_p(stream)))
+        shape = tuple(src.shape)
+        return means.view(*shape, 8), sel.view(shape)
+
+    def sat(self, src, stream=None):
+        import torch
+
+        x, batch, h, w = _as_batch(src)
+        c = torch.empty((batch, h + 1, w + 1), dtype=torch.float64, device=x.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        _check(self._lib.osbf_gpu_sat(
+            self.handle, _dtype_code(x), ctypes.c_void_p(x.data_ptr()), x.stride(1), x.stride(0),
+            w, h, batch, ctypes.c_void_p(c.data_ptr()), ctypes.c_void_p(stream)))
+        return c.view(*src.shape[:-2], h + 1, w + 1)
+
+    # -- host arrays (the drop-in path: H2D, filter, D2H inside the call) ----
+    def osbf_host(self, planes: np.ndarray, radius: int, iterations: int, mode="exact",
+                  out: np.ndarray | None = None) -> np.ndarray:
+        p = np.ascontiguousarray(planes)
+        code = {np.dtype(np.uint8): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2}.get(p.dtype)
+        if code is None:
+            p = p.astype(np.float64)
+            code = 2
+        if p.ndim == 2:
+            batch, (h, w) = 1, p.shape
+        elif p.ndim == 3:
+            batch, h, w = p.shape
+        else:
+            raise InvalidArgument("expected a (H, W) or (B, H, W) array")
+        if out is None:
+            out = np.empty(p.shape, dtype=np.float64)
+        _check(self._lib.osbf_gpu_osbf_host(
+            self.handle, code, ctypes.c_void_p(p.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+            w, h, batch, radius, iterations, _mode_code(mode)))
+        return out
+
+    def osbf_step_host(self, plane: np.ndarray, radius: int, mode="exact") -> np.ndarray:
+        p = np.ascontiguousarray(plane, dtype=np.float64)
+        if p.ndim != 2:
+            raise InvalidArgument("expected a (H, W) plane")
+        h, w = p.shape
+        out = np.empty_like(p)
+        _check(self._lib.osbf_gpu_osbf_step_host(
+            self.handle, ctypes.c_void_p(p.ctypes.data), ctypes.c_void_p(out.ctypes.data), w, h,
+            radius, _mode_code(mode)))
+        return out
+
+    def filter_multichannel_host(self, channels, radius: int, iterations: int, mode="exact",
+                                 outs=None):
+        chans = [np.ascontiguousarray(c, dtype=np.float64) for c in channels]
+        if not chans:
+            raise InvalidArgument("MultiChannelImage: channel count must be in [1,4]")
+        h, w = chans[0].shape
+        for c in chans:
+            if c.shape != (h, w):
+                raise InvalidArgument("MultiChannelImage: channel dimensions differ")
+        if outs is None:
+            outs = [np.empty((h, w), dtype=np.float64) for _ in chans]
+        ins = (ctypes.c_void_p * len(chans))(*[c.ctypes.data for c in chans])
+        ous = (ctypes.c_void_p * len(chans))(*[o.ctypes.data for o in outs])
+        _check(self._lib.osbf_gpu_filter_multichannel_host(
+            self.handle, ins, ous, len(chans), w, h, radius, iterations, _mode_code(mode)))
+        return outs
+
+    def sat_host(self, plane: np.ndarray) -> np.ndarray:
+        p = np.ascontiguousarray(plane, dtype=np.float64)
+        h, w = p.shape
+        c = np.empty((h + 1, w + 1), dtype=np.float64)
+        _check(self._lib.osbf_gpu_sat_host(self.handle, ctypes.c_void_p(p.ctypes.data), w, h,
+                                           ctypes.c_void_p(c.ctypes.data)))
+        return c
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    code = {torch.uint8: 0, torch.float32: 1, torch.float64: 2}.get(t.dtype)
+    if code is None:
+        raise InvalidArgument(f"unsupported dtype {t.dtype}")
+    return code
+
+
+def _as_batch(src):
+    if not getattr(src, "is_cuda", False):
+        raise InvalidArgument("expected a CUDA tensor (use the *_host methods for host arrays)")
+    if src.dim() == 2:
+        x = src.unsqueeze(0)
+    elif src.dim() == 3:
+        x = src
+    else:
+        raise InvalidArgument("expected a (H, W) or (B, H, W) tensor")
+    if x.stride(2) != 1:
+        x = x.contiguous()
+    b, h, w = x.shape
+    if h < 1 or w < 1:
+        raise InvalidArgument("ImagePlane: dimensions must be >= 1")
+    return x, b, h, w
+
+
+_default = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctxs = getattr(_default, "ctxs", None)
+    if ctxs is None:
+        ctxs = _default.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+# ---------------------------------------------------------------------------
+# reference free functions
+
+
+def _is_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and hasattr(x, "data_ptr")
+
+
+def osbf(plane, r: int, iterations: int, mode="exact"):
+    """filters2d.hpp:91-98 — ``iterations`` Jacobi passes of osbf_step.
+
+    ``iterations < 0`` raises InvalidArgument; ``iterations == 0`` returns a
+    copy without checking ``r`` (the reference's behaviour)."""
+    if _is_tensor(plane):
+        return default_context(plane.device.index or 0).iterate(plane, r, iterations, mode)
+    return default_context().osbf_host(np.asarray(plane), r, iterations, mode)
+
+
+def osbf_step(plane, r: int, mode="exact"):
+    """filters2d.hpp:61-88 — one pass; always validates ``r``."""
+    if r < 1:
+        raise InvalidArgument("osbf_step: radius must be >= 1")
+    return osbf(plane, r, 1, mode)
+
+
+def filter_multichannel(channels, config: FilterConfig, mode="exact"):
+    """filters2d.hpp:371-400, OsbfExact branch: channels filtered independently."""
+    config.validate()
+    if config.variant is not FilterVariant.OsbfExact:
+        raise InvalidArgument(
+            f"filter_multichannel: variant {config.variant.name} is not on the GPU OSBF path")
+    chans = list(channels) if not (hasattr(channels, "ndim") and channels.ndim == 3) else channels
+    if len(chans) < 1 or len(chans) > 4:
+        raise InvalidArgument("MultiChannelImage: channel count must be in [1,4]")
+    if _is_tensor(chans) or (len(chans) and _is_tensor(chans[0])):
+        import torch
+
+        stack = chans if _is_tensor(chans) else torch.stack(list(chans))
+        return default_context(stack.device.index or 0).iterate(
+            stack, config.radius, config.iterations, mode)
+    return default_context().filter_multichannel_host(chans, config.radius, config.iterations,
+                                                      mode)
+
+
+def build_sat(plane):
+    """integral.hpp:16-30 — the (H+1) x (W+1) summed-area table, built on the GPU."""
+    if _is_tensor(plane):
+        return default_context(plane.device.index or 0).sat(plane)
+    return default_context().sat_host(np.asarray(plane))
+
+
+def subwindow_means(plane, r: int, mode="exact"):
+    """filters2d.hpp:26-34 at every pixel: returns (means[..., 8], selected_id)."""
+    if r < 1:
+        raise InvalidArgument("sub_windows: radius must be >= 1")
+    if _is_tensor(plane):
+        return default_context(plane.device.index or 0).subwindow_means(plane, r, mode)
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(plane)).cuda()
+    m, s = default_context().subwindow_means(t, r, mode)
+    return m.cpu().numpy(), s.cpu().numpy()

@@ -1,0 +1,440 @@
+// C ABI of libosbf_gpu.so (include/osbf_gpu.h): contexts, argument validation
+// with the reference's error behaviour, the Jacobi iteration driver and the
+// host-buffer entry points used by the drop-in C++ headers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "osbf_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+osbf_status fail(osbf_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+osbf_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? OSBF_ERR_ALLOC : OSBF_ERR_CUDA, "%s: %s (%s)",
+                where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define OSBF_CUDA(call, where)                         \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+size_t dtype_size(osbf_dtype d) {
+    switch (d) {
+        case OSBF_U8: return 1;
+        case OSBF_F32: return 4;
+        default: return 8;
+    }
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&ptr, need);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+}  // namespace
+
+struct osbf_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf ping, pong;         // fp64 Jacobi planes
+    DevBuf rowpfx, sat;        // exact-mode workspace
+    DevBuf host_in, host_out;  // staging for the host entry points
+    osbf_gpu::LaunchCounter lc;
+};
+
+namespace {
+
+int device_ok_cached = -1;
+std::mutex device_mu;
+
+bool device_ok() {
+    std::lock_guard<std::mutex> lock(device_mu);
+    if (device_ok_cached >= 0) return device_ok_cached == 1;
+    int n = 0;
+    device_ok_cached = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, 0) == cudaSuccess && prop.major == 10) device_ok_cached = 1;
+    return device_ok_cached == 1;
+}
+
+osbf_status check_geometry(int width, int height, int batch) {
+    if (width < 1 || height < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "ImagePlane: dimensions must be >= 1");
+    if (batch < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+    return OSBF_OK;
+}
+
+osbf_status check_dtype(osbf_dtype d) {
+    if (d != OSBF_U8 && d != OSBF_F32 && d != OSBF_F64)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown dtype %d", static_cast<int>(d));
+    return OSBF_OK;
+}
+
+osbf_status check_mode(osbf_mode m) {
+    if (m != OSBF_MODE_EXACT && m != OSBF_MODE_FAST)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown mode %d", static_cast<int>(m));
+    return OSBF_OK;
+}
+
+cudaStream_t pick_stream(osbf_ctx* ctx, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+}
+
+// One pass in the requested mode: src (typed view) -> dst (fp64).
+osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
+                     int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
+                     osbf_mode mode, cudaStream_t s) {
+    if (mode == OSBF_MODE_EXACT) {
+        const size_t n = static_cast<size_t>(g.batch) * g.width * g.height;
+        const size_t ns = static_cast<size_t>(g.batch) * (g.width + 1) * (g.height + 1);
+        OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");
+        OSBF_CUDA(ctx->sat.ensure(ns * sizeof(double)), "alloc sat");
+        OSBF_CUDA(osbf_gpu::exact_build_sat(src, g, ctx->rowpfx.as<double>(), ctx->sat.as<double>(),
+                                            s, ctx->lc),
+                  "exact SAT");
+        OSBF_CUDA(osbf_gpu::exact_select(src, g, r, ctx->sat.as<double>(), dst, dp, dpl, means, sel,
+                                         s, ctx->lc),
+                  "exact select");
+    } else {
+        OSBF_CUDA(osbf_gpu::fast_step(src, g, r, dst, dp, dpl, means, sel, s, ctx->lc),
+                  "fast step");
+    }
+    return OSBF_OK;
+}
+
+// Copy/convert kernel: typed batch -> fp64 batch.
+template <typename T>
+__global__ void convert_kernel(const T* __restrict__ in, size_t ip, size_t ipl,
+                               double* __restrict__ out, size_t op, size_t opl, int W, int H) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int b = blockIdx.z;
+    if (x >= W) return;
+    out[b * opl + static_cast<size_t>(y) * op + x] =
+        static_cast<double>(in[b * ipl + static_cast<size_t>(y) * ip + x]);
+}
+
+}  // namespace
+
+namespace osbf_gpu {
+cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                           size_t opl, cudaStream_t s, LaunchCounter& lc) {
+    dim3 grid((g.width + 255) / 256, g.height, g.batch);
+    ++lc.launches;
+    switch (in.dtype) {
+        case OSBF_U8:
+            convert_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(in.base), in.pitch,
+                                                in.plane, out, op, opl, g.width, g.height);
+            break;
+        case OSBF_F32:
+            convert_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(in.base), in.pitch,
+                                                in.plane, out, op, opl, g.width, g.height);
+            break;
+        default:
+            convert_kernel<<<grid, 256, 0, s>>>(static_cast<const double*>(in.base), in.pitch,
+                                                in.plane, out, op, opl, g.width, g.height);
+            break;
+    }
+    return cudaGetLastError();
+}
+}  // namespace osbf_gpu
+
+extern "C" {
+
+int osbf_gpu_abi_version(void) { return OSBF_GPU_ABI_VERSION; }
+
+const char* osbf_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int osbf_gpu_device_available(void) { return device_ok() ? 1 : 0; }
+
+osbf_status osbf_gpu_ctx_create(int device, osbf_ctx** out) {
+    if (!out) return fail(OSBF_ERR_INVALID_ARGUMENT, "ctx_create: null out pointer");
+    *out = nullptr;
+    if (!device_ok()) return fail(OSBF_ERR_NO_DEVICE, "no CUDA device of compute capability 10.x");
+    OSBF_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    osbf_ctx* ctx = new (std::nothrow) osbf_ctx();
+    if (!ctx) return fail(OSBF_ERR_ALLOC, "ctx_create: out of host memory");
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    *out = ctx;
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx) {
+    if (!ctx) return OSBF_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->ping.release();
+    ctx->pong.release();
+    ctx->rowpfx.release();
+    ctx->sat.release();
+    ctx->host_in.release();
+    ctx->host_out.release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_ctx_trim(osbf_ctx* ctx) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    cudaSetDevice(ctx->device);
+    OSBF_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->ping.release();
+    ctx->pong.release();
+    ctx->rowpfx.release();
+    ctx->sat.release();
+    ctx->host_in.release();
+    ctx->host_out.release();
+    return OSBF_OK;
+}
+
+uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx) { return ctx ? ctx->lc.launches : 0; }
+
+osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                             size_t in_pitch, size_t in_plane_stride, double* d_out,
+                             size_t out_pitch, size_t out_plane_stride, int width, int height,
+                             int batch, int radius, int iterations, osbf_mode mode,
+                             void* stream) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if ((st = check_mode(mode)) != OSBF_OK) return st;
+    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf: iterations must be >= 0");
+    if (iterations > 0 && radius < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+    if (!d_in || !d_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null plane pointer");
+    if (in_pitch < static_cast<size_t>(width) || out_pitch < static_cast<size_t>(width))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "pitch smaller than width");
+    if (batch > 1 && (in_plane_stride < in_pitch * height || out_plane_stride < out_pitch * height))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "plane stride smaller than pitch*height");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = pick_stream(ctx, stream);
+
+    const osbf_gpu::Geometry g{width, height, batch};
+    const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_plane_stride};
+    if (iterations == 0) {
+        // filters2d.hpp:94-97: a copy, radius unchecked.
+        if (static_cast<const void*>(d_out) == d_in && in_dtype == OSBF_F64) return OSBF_OK;
+        OSBF_CUDA(osbf_gpu::convert_to_f64(input, g, d_out, out_pitch, out_plane_stride, s, ctx->lc),
+                  "copy");
+        return OSBF_OK;
+    }
+    // Jacobi ping-pong through context scratch; the last pass writes d_out.
+    const size_t plane = static_cast<size_t>(width) * height;
+    const bool alias = static_cast<const void*>(d_out) == d_in;
+    const int scratch_needed = (iterations > 1 ? 2 : 0) + (alias ? 1 : 0);
+    if (scratch_needed > 0) OSBF_CUDA(ctx->ping.ensure(plane * batch * sizeof(double)), "alloc ping");
+    if (scratch_needed > 1) OSBF_CUDA(ctx->pong.ensure(plane * batch * sizeof(double)), "alloc pong");
+    osbf_gpu::PlaneView src = input;
+    for (int it = 0; it < iterations; ++it) {
+        const bool last = it == iterations - 1;
+        double* dst;
+        size_t dp, dpl;
+        if (last && !alias) {
+            dst = d_out;
+            dp = out_pitch;
+            dpl = out_plane_stride;
+        } else {
+            DevBuf& buf = (it % 2 == 0) ? ctx->ping : ctx->pong;
+            dst = buf.as<double>();
+            dp = width;
+            dpl = plane;
+        }
+        if ((st = one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s)) != OSBF_OK)
+            return st;
+        src = osbf_gpu::PlaneView{dst, OSBF_F64, dp, dpl};
+    }
+    if (alias) {
+        OSBF_CUDA(cudaMemcpy2DAsync(d_out, out_pitch * sizeof(double), src.base,
+                                    src.pitch * sizeof(double), width * sizeof(double),
+                                    static_cast<size_t>(height) * batch, cudaMemcpyDeviceToDevice, s),
+                  "copy back");
+    }
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                                     size_t in_pitch, size_t in_plane_stride, int width,
+                                     int height, int batch, int radius, double* d_means,
+                                     uint8_t* d_sel, osbf_mode mode, void* stream) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if ((st = check_mode(mode)) != OSBF_OK) return st;
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "sub_windows: radius must be >= 1");
+    if (!d_in) return fail(OSBF_ERR_INVALID_ARGUMENT, "null plane pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = pick_stream(ctx, stream);
+    const osbf_gpu::Geometry g{width, height, batch};
+    const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_plane_stride};
+    return one_pass(ctx, input, g, radius, nullptr, 0, 0, d_means, d_sel, mode, s);
+}
+
+osbf_status osbf_gpu_sat(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in, size_t in_pitch,
+                         size_t in_plane_stride, int width, int height, int batch,
+                         double* d_cumsum, void* stream) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if (!d_in || !d_cumsum) return fail(OSBF_ERR_INVALID_ARGUMENT, "null pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = pick_stream(ctx, stream);
+    const osbf_gpu::Geometry g{width, height, batch};
+    const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_plane_stride};
+    OSBF_CUDA(ctx->rowpfx.ensure(static_cast<size_t>(batch) * width * height * sizeof(double)),
+              "alloc row prefix");
+    OSBF_CUDA(osbf_gpu::exact_build_sat(input, g, ctx->rowpfx.as<double>(), d_cumsum, s, ctx->lc),
+              "exact SAT");
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                               double* h_out, int width, int height, int batch, int radius,
+                               int iterations, osbf_mode mode) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf: iterations must be >= 0");
+    if (iterations > 0 && radius < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+    if (!h_in || !h_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t n = static_cast<size_t>(width) * height * batch;
+    OSBF_CUDA(ctx->host_in.ensure(n * dtype_size(in_dtype)), "alloc input");
+    OSBF_CUDA(ctx->host_out.ensure(n * sizeof(double)), "alloc output");
+    cudaStream_t s = ctx->stream;
+    OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * dtype_size(in_dtype),
+                              cudaMemcpyHostToDevice, s),
+              "H2D");
+    const size_t plane = static_cast<size_t>(width) * height;
+    st = osbf_gpu_iterate(ctx, in_dtype, ctx->host_in.ptr, width, plane, ctx->host_out.as<double>(),
+                          width, plane, width, height, batch, radius, iterations, mode, s);
+    if (st != OSBF_OK) return st;
+    OSBF_CUDA(cudaMemcpyAsync(h_out, ctx->host_out.ptr, n * sizeof(double), cudaMemcpyDeviceToHost,
+                              s),
+              "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_osbf_step_host(osbf_ctx* ctx, const double* h_in, double* h_out, int width,
+                                    int height, int radius, osbf_mode mode) {
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+    return osbf_gpu_osbf_host(ctx, OSBF_F64, h_in, h_out, width, height, 1, radius, 1, mode);
+}
+
+osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const* h_in,
+                                              double* const* h_out, int channels, int width,
+                                              int height, int radius, int iterations,
+                                              osbf_mode mode) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    // FilterConfig::validate (core.hpp:244-253), then the channel checks of
+    // MultiChannelImage (core.hpp:85-92).
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "FilterConfig: radius must be >= 1");
+    if (iterations < 0)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "FilterConfig: iterations must be >= 0");
+    if (channels < 1 || channels > 4)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "MultiChannelImage: channel count must be in [1,4]");
+    osbf_status st;
+    if ((st = check_geometry(width, height, 1)) != OSBF_OK) return st;
+    if (!h_in || !h_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t plane = static_cast<size_t>(width) * height;
+    OSBF_CUDA(ctx->host_in.ensure(plane * channels * sizeof(double)), "alloc input");
+    OSBF_CUDA(ctx->host_out.ensure(plane * channels * sizeof(double)), "alloc output");
+    cudaStream_t s = ctx->stream;
+    double* din = ctx->host_in.as<double>();
+    double* dout = ctx->host_out.as<double>();
+    for (int c = 0; c < channels; ++c) {
+        if (!h_in[c] || !h_out[c]) return fail(OSBF_ERR_INVALID_ARGUMENT, "null channel pointer");
+        OSBF_CUDA(cudaMemcpyAsync(din + c * plane, h_in[c], plane * sizeof(double),
+                                  cudaMemcpyHostToDevice, s),
+                  "H2D");
+    }
+    // Channels are independent (filters2d.hpp:376-384): one batched launch.
+    st = osbf_gpu_iterate(ctx, OSBF_F64, din, width, plane, dout, width, plane, width, height,
+                          channels, radius, iterations, mode, s);
+    if (st != OSBF_OK) return st;
+    for (int c = 0; c < channels; ++c)
+        OSBF_CUDA(cudaMemcpyAsync(h_out[c], dout + c * plane, plane * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s),
+                  "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+
+osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,
+                              double* h_cumsum) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, 1)) != OSBF_OK) return st;
+    if (!h_in || !h_cumsum) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t plane = static_cast<size_t>(width) * height;
+    const size_t ns = static_cast<size_t>(width + 1) * (height + 1);
+    OSBF_CUDA(ctx->host_in.ensure(plane * sizeof(double)), "alloc input");
+    OSBF_CUDA(ctx->host_out.ensure(ns * sizeof(double)), "alloc output");
+    cudaStream_t s = ctx->stream;
+    OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, plane * sizeof(double), cudaMemcpyHostToDevice,
+                              s),
+              "H2D");
+    st = osbf_gpu_sat(ctx, OSBF_F64, ctx->host_in.ptr, width, plane, width, height, 1,
+                      ctx->host_out.as<double>(), s);
+    if (st != OSBF_OK) return st;
+    OSBF_CUDA(cudaMemcpyAsync(h_cumsum, ctx->host_out.ptr, ns * sizeof(double),
+                              cudaMemcpyDeviceToHost, s),
+              "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+
+}  // extern "C"

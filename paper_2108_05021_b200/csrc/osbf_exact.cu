@@ -1,0 +1,192 @@
+// Exact mode: bit-identical replay of the reference OSBF pass.
+//
+// The reference (integral.hpp:16-30) builds ONE whole-image fp64 summed-area
+// table with a serial left-to-right running row sum, adding the table row
+// above:  C(x+1,y+1) = C(x+1,y) + R(x,y),  R(x,y) = R(x-1,y) + U(x,y).
+// Every later rounding depends on that order, and the selection's strict-<
+// tie-break (filters2d.hpp:72-82) decides exact ties through that rounding
+// noise, so this mode reproduces the order exactly:
+//   K1 exact_row_prefix : R, one serial fp64 chain per row (H*B chains),
+//                         coalesced through a per-warp shared-memory transpose;
+//   K2 exact_col_chain  : C, one serial fp64 chain per table column;
+//   K3 exact_stencil    : per pixel, 8 clipped ((A-B)-C)+D sums
+//                         (integral.hpp:48-49), IEEE division by the valid
+//                         count (integral.hpp:68), |a-u|, strict < in window
+//                         order, write a_m itself (filters2d.hpp:80-83).
+// All fp64 arithmetic uses the _rn intrinsics so nothing is contracted.
+#include "osbf_internal.cuh"
+
+namespace osbf_gpu {
+namespace {
+
+constexpr int kRowWarps = 4;   // warps per CTA in K1
+constexpr int kChunk = 32;     // columns per transpose chunk
+
+template <typename T>
+__global__ void __launch_bounds__(kRowWarps * 32)
+    exact_row_prefix(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
+                     double* __restrict__ rowpfx, int W, int H, long long total_rows) {
+    __shared__ double tile[kRowWarps][kChunk][kChunk + 1];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const long long row0 = (static_cast<long long>(blockIdx.x) * kRowWarps + warp) * 32;
+    if (row0 >= total_rows) return;
+    double (*t)[kChunk + 1] = tile[warp];
+
+    // Element offset of row (row0 + lane); broadcast per row inside the loads.
+    long long my_base = -1;
+    {
+        const long long g = row0 + lane;
+        if (g < total_rows) {
+            const long long b = g / H, y = g - b * H;
+            my_base = b * static_cast<long long>(in_plane) + y * static_cast<long long>(in_pitch);
+        }
+    }
+    double acc = 0.0;
+    for (int x0 = 0; x0 < W; x0 += kChunk) {
+        const int x = x0 + lane;
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const long long base = __shfl_sync(0xffffffffu, my_base, rr);
+            double v = 0.0;
+            if (base >= 0 && x < W) v = to_f64(in[base + x]);
+            t[rr][lane] = v;
+        }
+        __syncwarp();
+        const int n = min(kChunk, W - x0);
+        for (int c = 0; c < n; ++c) {
+            acc = __dadd_rn(acc, t[lane][c]);  // row += src[x]  (integral.hpp:25)
+            t[lane][c] = acc;
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const long long g = row0 + rr;
+            if (g < total_rows && x < W) rowpfx[g * W + x] = t[rr][lane];
+        }
+        __syncwarp();
+    }
+}
+
+// One thread per table column cx in [0, W] of each plane.
+__global__ void exact_col_chain(const double* __restrict__ rowpfx, double* __restrict__ sat,
+                                int W, int H, int B) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long cols = static_cast<long long>(W) + 1;
+    if (t >= cols * B) return;
+    const long long b = t / cols;
+    const int cx = static_cast<int>(t - b * cols);
+    double* C = sat + b * cols * (H + 1);
+    C[cx] = 0.0;  // zero border row
+    if (cx == 0) {
+        for (int cy = 1; cy <= H; ++cy) C[static_cast<long long>(cy) * cols] = 0.0;
+        return;
+    }
+    const double* R = rowpfx + b * static_cast<long long>(W) * H + (cx - 1);
+    double acc = 0.0;
+#pragma unroll 8
+    for (int y = 0; y < H; ++y) {
+        acc = __dadd_rn(acc, R[static_cast<long long>(y) * W]);  // above[x+1] + row (integral.hpp:26)
+        C[static_cast<long long>(y + 1) * cols + cx] = acc;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    exact_stencil(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
+                  const double* __restrict__ sat, double* __restrict__ out, size_t out_pitch,
+                  size_t out_plane, double* __restrict__ means, uint8_t* __restrict__ sel, int W,
+                  int H, int r) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int b = blockIdx.z;
+    if (x >= W || y >= H) return;
+    const long long cols = static_cast<long long>(W) + 1;
+    const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
+    const double u = to_f64(in[b * in_plane + static_cast<size_t>(y) * in_pitch + x]);
+    double best = 0.0;
+    double best_abs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    int best_id = 0;
+    const size_t pix = (static_cast<size_t>(b) * H + y) * W + x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const Win w = window(i, r);
+        const int x0 = max(x + w.u0, 0), x1 = min(x + w.u1, W - 1);
+        const int y0 = max(y + w.v0, 0), y1 = min(y + w.v1, H - 1);
+        const long long n = static_cast<long long>(x1 - x0 + 1) * (y1 - y0 + 1);
+        const double A = C[(y1 + 1) * cols + (x1 + 1)];
+        const double Bv = C[(y1 + 1) * cols + x0];
+        const double Cv = C[y0 * cols + (x1 + 1)];
+        const double D = C[y0 * cols + x0];
+        const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
+        const double a = __ddiv_rn(s, static_cast<double>(n));
+        if (means) means[pix * 8 + i] = a;
+        const double d = fabs(__dsub_rn(a, u));
+        if (d < best_abs) {
+            best_abs = d;
+            best = a;
+            best_id = i + 1;
+        }
+    }
+    if (out) out[b * out_plane + static_cast<size_t>(y) * out_pitch + x] = best;
+    if (sel) sel[pix] = static_cast<uint8_t>(best_id);
+}
+
+template <typename T>
+cudaError_t launch_row_prefix(const PlaneView& in, const Geometry& g, double* rowpfx,
+                              cudaStream_t s) {
+    const long long rows = static_cast<long long>(g.batch) * g.height;
+    const long long warps = (rows + 31) / 32;
+    const unsigned blocks = static_cast<unsigned>((warps + kRowWarps - 1) / kRowWarps);
+    exact_row_prefix<T><<<blocks, kRowWarps * 32, 0, s>>>(
+        static_cast<const T*>(in.base), in.pitch, in.plane, rowpfx, g.width, g.height, rows);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const double* sat,
+                           double* out, size_t op, size_t opl, double* means, uint8_t* sel,
+                           cudaStream_t s) {
+    dim3 grid((g.width + 31) / 32, (g.height + 7) / 8, g.batch);
+    exact_stencil<T><<<grid, 256, 0, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane, sat,
+                                          out, op, opl, means, sel, g.width, g.height, r);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
+                            cudaStream_t s, LaunchCounter& lc) {
+    cudaError_t e;
+    switch (in.dtype) {
+        case OSBF_U8: e = launch_row_prefix<uint8_t>(in, g, rowpfx, s); break;
+        case OSBF_F32: e = launch_row_prefix<float>(in, g, rowpfx, s); break;
+        default: e = launch_row_prefix<double>(in, g, rowpfx, s); break;
+    }
+    ++lc.launches;
+    if (e != cudaSuccess) return e;
+    const long long threads = (static_cast<long long>(g.width) + 1) * g.batch;
+    exact_col_chain<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(
+        rowpfx, sat, g.width, g.height, g.batch);
+    ++lc.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
+                         double* out, size_t out_pitch, size_t out_plane, double* means,
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc) {
+    ++lc.launches;
+    switch (in.dtype) {
+        case OSBF_U8:
+            return launch_stencil<uint8_t>(in, g, radius, sat, out, out_pitch, out_plane, means,
+                                           sel, s);
+        case OSBF_F32:
+            return launch_stencil<float>(in, g, radius, sat, out, out_pitch, out_plane, means, sel,
+                                         s);
+        default:
+            return launch_stencil<double>(in, g, radius, sat, out, out_pitch, out_plane, means,
+                                          sel, s);
+    }
+}
+
+}  // namespace osbf_gpu

@@ -1,0 +1,86 @@
+// Internal declarations shared by the OSBF kernels and the C ABI layer.
+// Not installed; the public surface is include/osbf_gpu.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "osbf_gpu.h"
+
+namespace osbf_gpu {
+
+// A batch of planes in device memory: sample(b,x,y) = base[b*plane + y*pitch + x].
+struct PlaneView {
+    const void* base;
+    osbf_dtype dtype;
+    size_t pitch;  // elements
+    size_t plane;  // elements
+};
+
+struct Geometry {
+    int width;
+    int height;
+    int batch;
+};
+
+// Launch statistics (kernels issued) for instrumentation.
+struct LaunchCounter {
+    uint64_t launches = 0;
+};
+
+// ---- exact mode (osbf_exact.cu) ------------------------------------------
+// Whole-image summed-area table in the reference's serial order.
+//   rowpfx: fp64 [batch][height][width] workspace (row running sums)
+//   sat   : fp64 [batch][height+1][width+1]
+cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
+                            cudaStream_t s, LaunchCounter& lc);
+// One exact OSBF pass reading `in` and the SAT built from it.
+//   out   : fp64 (nullable), out_pitch / out_plane in elements
+//   means : fp64 [batch][height][width][8] (nullable)
+//   sel   : uint8 [batch][height][width] (nullable)
+cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
+                         double* out, size_t out_pitch, size_t out_plane, double* means,
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc);
+
+// ---- fast mode (osbf_fast.cu) --------------------------------------------
+// One OSBF pass with tile-local fp64 summed-area tables.
+cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double* out,
+                      size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
+                      cudaStream_t s, LaunchCounter& lc);
+
+// ---- utilities (osbf_capi.cu) ----------------------------------------------
+cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t out_pitch,
+                           size_t out_plane, cudaStream_t s, LaunchCounter& lc);
+
+}  // namespace osbf_gpu
+
+// Device helpers -----------------------------------------------------------
+#ifdef __CUDACC__
+namespace osbf_gpu {
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v) {
+    return static_cast<double>(v);  // exact for u8, f32, f64
+}
+
+// Reference window table (core.hpp:212-225) in selection order.
+// u = column offset, v = row offset; +v is the next row in memory.
+struct Win {
+    int u0, u1, v0, v1;
+};
+__device__ __forceinline__ Win window(int i, int r) {
+    switch (i) {
+        case 0: return {-r, 0, 0, r};
+        case 1: return {0, r, 0, r};
+        case 2: return {0, r, -r, 0};
+        case 3: return {-r, 0, -r, 0};
+        case 4: return {-r, 0, -r, r};
+        case 5: return {0, r, -r, r};
+        case 6: return {-r, r, 0, r};
+        default: return {-r, r, -r, 0};
+    }
+}
+
+}  // namespace osbf_gpu
+#endif

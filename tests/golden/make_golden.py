@@ -1,0 +1,99 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref).
+
+The reference repository ships no golden files — its tests generate every
+input from seeds (proj/tests/support/fixtures.hpp:15-71).  This script runs
+the reference itself (its headers compiled behind oracle/ref_shim.cpp) on
+seeded inputs and stores inputs + outputs, so the C restatement and the GPU
+path can be pinned against real reference outputs on machines where the
+reference tree is absent (the GPU box).
+
+    python tests/golden/make_golden.py          # rewrites the .npz files
+
+Cases mirror the reference's own hot-path tests (file:line under
+/root/reference/proj/tests/) plus the BASELINE configs at reduced size.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.abspath(os.path.join(HERE, "..", ".."))
+sys.path.insert(0, ROOT)
+
+from oracle import Reference  # noqa: E402
+from paper_2108_05021_b200 import synth  # noqa: E402
+
+
+def random_plane(h, w, seed, lo=0.0, hi=255.0):
+    rng = np.random.default_rng(seed)
+    return lo + (hi - lo) * rng.random((h, w))
+
+
+def checkerboard(w, h, cell, lo, hi):
+    y, x = np.mgrid[0:h, 0:w]
+    return np.where(((x // cell + y // cell) % 2) == 0, lo, hi).astype(np.float64)
+
+
+def step(w, h, edge, lo, hi):
+    x = np.arange(w)[None, :].repeat(h, 0)
+    return np.where(x < edge, lo, hi).astype(np.float64)
+
+
+def cases():
+    """(name, input (H,W) or (C,H,W), r, iterations)."""
+    out = []
+    # test_filters2d.cpp:142-147 — osbf vs brute force, 24x24, r in {1,2,3,5}, 3 iterations
+    for r in (1, 2, 3, 5):
+        out.append((f"random24_r{r}", random_plane(24, 24, 200 + r), r, 3))
+    # acceptance.cpp:137-152 — 64x64 planes, r in {1,2,3,5}, 3 iterations (2 of the 50)
+    for k in (0, 1):
+        for r in (1, 2, 3, 5):
+            out.append((f"random64_k{k}_r{r}", random_plane(64, 64, 1000 + k), r, 3))
+    # C3-style uint8 mosaic, radius sweep, 10 iterations (bit-exact target)
+    rng = np.random.default_rng(33)
+    u8 = synth.u8_mosaic(96, 80, rng, block=(4, 40))
+    for r in (1, 2, 4, 8, 16):
+        out.append((f"u8mosaic_r{r}", u8, r, 10))
+    # BASELINE C1 / C2 at reduced size (float32 inputs)
+    out.append(("c1_shrink4", synth.make_input("C1", shrink=4)[0], 2, 10))
+    out.append(("c2_shrink12", synth.make_input("C2", shrink=12), 3, 30))
+    # edge cases: degenerate shapes, windows wider than the image, fixed points
+    out.append(("one_px", np.array([[7.5]]), 2, 3))
+    out.append(("row_1x17", random_plane(1, 17, 5), 3, 2))
+    out.append(("col_13x1", random_plane(13, 1, 6), 2, 2))
+    out.append(("tiny_7x5_r16", random_plane(7, 5, 7), 16, 4))
+    out.append(("ragged_37x29_r4", random_plane(37, 29, 8), 4, 3))
+    out.append(("constant_9x9", np.full((9, 9), 3.5), 2, 1))
+    out.append(("step_32x16_r5", step(32, 16, 16, 0.0, 100.0), 5, 1))
+    out.append(("step_64x32_30it", step(64, 32, 32, 0.0, 100.0), 2, 30))
+    out.append(("checker_64_cell9_r3", checkerboard(64, 64, 9, 10.0, 200.0), 3, 1))
+    out.append(("checker_32_cell4_r3", checkerboard(32, 32, 4, 0.0, 255.0), 3, 1))
+    out.append(("zero_iters", random_plane(10, 10, 3), 2, 0))
+    out.append(("negative_values", random_plane(20, 20, 9, -1e3, 1e3), 2, 4))
+    return out
+
+
+def main() -> None:
+    ref = Reference()
+    ref.set_max_threads(1)
+    for name, inp, r, iters in cases():
+        if inp.ndim == 3:
+            out = ref.filter_multichannel(inp.astype(np.float64), r, iters)
+            means, sel = ref.subwindow_means(inp[0].astype(np.float64), r)
+        else:
+            out = ref.osbf(inp.astype(np.float64), r, iters)
+            means, sel = ref.subwindow_means(inp.astype(np.float64), r)
+        extra = {"step1_means": means} if means.shape[0] * means.shape[1] <= 1024 else {}
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), input=inp, output=out,
+                            radius=r, iterations=iters, step1_sel=sel, **extra)
+        print(f"{name:24s} in {inp.shape} {inp.dtype} r={r} it={iters}")
+    # integral.hpp / test_integral.cpp:19-29 known SAT
+    p = np.array([[1.0, 2.0], [3.0, 4.0]])
+    np.savez_compressed(os.path.join(HERE, "sat_2x2.npz"), input=p, cumsum=ref.sat(p))
+
+
+if __name__ == "__main__":
+    main()

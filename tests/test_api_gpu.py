@@ -1,0 +1,72 @@
+"""Reference-interface behaviour of the Python mirror on the GPU: error
+types, zero-iteration quirk, multichannel semantics (filters2d.hpp:371-400)."""
+import numpy as np
+import pytest
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def test_error_behaviour_matches_reference():
+    import paper_2108_05021_b200 as ob
+
+    p = np.random.default_rng(1).random((8, 8))
+    with pytest.raises(ob.InvalidArgument):
+        ob.osbf_step(p, 0)  # filters2d.hpp:62-63
+    with pytest.raises(ob.InvalidArgument):
+        ob.osbf(p, 0, 1)
+    with pytest.raises(ob.InvalidArgument):
+        ob.osbf(p, 2, -1)  # filters2d.hpp:92-93
+    # iterations == 0 copies without validating r (filters2d.hpp:94-97)
+    assert np.array_equal(ob.osbf(p, 0, 0), p)
+    assert np.array_equal(ob.osbf(p, -5, 0), p)
+    with pytest.raises(ob.InvalidArgument):
+        ob.osbf(np.zeros((0, 4)), 2, 1)  # core.hpp:20-21
+    ctx = ob.default_context()
+    st = ctx._lib.osbf_gpu_osbf_step_host(ctx.handle, None, None, 4, 4, 0, 0)
+    assert st == 1 and b"radius must be >= 1" in ctx._lib.osbf_gpu_last_error()
+
+
+def test_multichannel_semantics():
+    import paper_2108_05021_b200 as ob
+
+    cfg = ob.FilterConfig(radius=2, iterations=2)
+    flat = [np.full((12, 12), v) for v in (1.0, 2.0, 3.0)]
+    out = ob.filter_multichannel(flat, cfg)
+    for o, c in zip(out, flat):
+        assert np.array_equal(o, c)
+    rng = np.random.default_rng(2)
+    rgb = [rng.random((12, 12)) * 255 for _ in range(3)]
+    filtered = ob.filter_multichannel(rgb, cfg)
+    for f, c in zip(filtered, rgb):
+        assert np.array_equal(bits(f), bits(ob.osbf(c, 2, 2)))
+    with pytest.raises(ob.InvalidArgument):
+        ob.filter_multichannel(rgb, ob.FilterConfig(radius=0))
+    with pytest.raises(ob.InvalidArgument):
+        ob.filter_multichannel(rgb * 2, cfg)  # 6 channels
+    with pytest.raises(ob.InvalidArgument):
+        ob.filter_multichannel(rgb, ob.FilterConfig(variant=ob.FilterVariant.Box))
+
+
+def test_launch_counter_counts_kernels(ctx):
+    import torch
+
+    x = torch.rand((64, 64), dtype=torch.float64, device="cuda")
+    before = ctx.launches
+    ctx.iterate(x, 2, 3, mode="exact")
+    assert ctx.launches - before == 9  # 3 kernels per exact pass
+    before = ctx.launches
+    ctx.iterate(x, 2, 3, mode="fast")
+    assert ctx.launches - before == 3
+
+
+def test_dtype_promotion_is_exact(ctx, oracle_lib):
+    import torch
+
+    rng = np.random.default_rng(4)
+    u8 = rng.integers(0, 256, (33, 45), dtype=np.uint8)
+    f32 = (rng.random((33, 45)) * 3).astype(np.float32)
+    for a in (u8, f32):
+        got = ctx.iterate(torch.from_numpy(a).cuda(), 2, 2, mode="exact").cpu().numpy()
+        assert np.array_equal(bits(got), bits(oracle_lib.osbf(a.astype(np.float64), 2, 2)))

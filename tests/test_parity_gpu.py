@@ -1,0 +1,191 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the reference's golden outputs.
+
+Bars (BASELINE.json north_star):
+  * exact mode: bit-identical output and selection to the reference on every
+    input, every iteration;
+  * fast mode: bit-identical whenever window sums are exact (integer inputs,
+    first pass); otherwise max-abs <= FLOAT_TOL * value range.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FLOAT_TOL = 1e-5  # north_star: max-abs error <= 1e-5 of the value range (float32 configs)
+
+
+def torch_dev(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def vrange(a):
+    a = np.asarray(a, dtype=np.float64)
+    return max(float(a.max() - a.min()), 1e-300)
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: os.path.basename(p)[:-4])
+def test_exact_matches_reference_golden(ctx, path):
+    g = load_golden(path)
+    inp, r, it = g["input"], int(g["radius"]), int(g["iterations"])
+    want = g["output"]
+    got = ctx.iterate(torch_dev(inp), r, it, mode="exact").cpu().numpy()
+    assert np.array_equal(bits(got), bits(want))
+    # host-buffer entry point (what the drop-in C++ API calls)
+    got_h = ctx.osbf_host(inp, r, it, mode="exact")
+    assert np.array_equal(bits(got_h), bits(want))
+    if it > 0:
+        first = inp if inp.ndim == 2 else inp[0]
+        means, sel = ctx.subwindow_means(torch_dev(first), r, mode="exact")
+        assert np.array_equal(sel.cpu().numpy(), g["step1_sel"])
+        if "step1_means" in g:
+            assert np.array_equal(bits(means.cpu().numpy()), bits(g["step1_means"]))
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: os.path.basename(p)[:-4])
+def test_fast_matches_reference_golden(ctx, path):
+    g = load_golden(path)
+    inp, r, it = g["input"], int(g["radius"]), int(g["iterations"])
+    got = ctx.iterate(torch_dev(inp), r, it, mode="fast").cpu().numpy()
+    want = g["output"]
+    if it == 0:
+        assert np.array_equal(bits(got), bits(want))
+        return
+    if inp.dtype == np.uint8 or np.all(inp == np.round(inp)):
+        # integer window sums are exact in any order: the first pass is bit-exact
+        first = inp if inp.ndim == 2 else inp[0]
+        one = ctx.iterate(torch_dev(first), r, 1, mode="fast").cpu().numpy()
+        import oracle
+
+        assert np.array_equal(bits(one), bits(oracle.Oracle().osbf(first, r, 1)))
+    if inp.dtype != np.uint8:
+        err = np.abs(got - want).max()
+        assert err <= FLOAT_TOL * vrange(inp), f"max abs err {err}"
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_exact_random_shapes_bit_exact(ctx, oracle_lib, seed):
+    rng = np.random.default_rng(100 + seed)
+    h, w = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+    r = int(rng.choice([1, 2, 3, 4, 7, 16]))
+    p = rng.random((h, w)) * 255.0
+    got = ctx.iterate(torch_dev(p), r, 3, mode="exact").cpu().numpy()
+    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, r, 3)))
+
+
+def test_exact_sat_bit_exact(ctx, oracle_lib):
+    rng = np.random.default_rng(7)
+    for h, w in [(1, 1), (3, 200), (257, 65), (300, 301)]:
+        p = rng.random((h, w)) * 1000 - 500
+        got = ctx.sat(torch_dev(p)).cpu().numpy()
+        assert np.array_equal(bits(got), bits(oracle_lib.sat(p)))
+        assert np.array_equal(bits(ctx.sat_host(p)), bits(oracle_lib.sat(p)))
+
+
+def test_config_c1_full(ctx, oracle_lib):
+    from paper_2108_05021_b200 import synth
+
+    cfg = synth.CONFIGS["C1"]
+    x = synth.make_input("C1")[0]
+    want = oracle_lib.osbf(x, cfg.radius, cfg.iterations)
+    exact = ctx.iterate(torch_dev(x), cfg.radius, cfg.iterations, mode="exact").cpu().numpy()
+    assert np.array_equal(bits(exact), bits(want))
+    fast = ctx.iterate(torch_dev(x), cfg.radius, cfg.iterations, mode="fast").cpu().numpy()
+    assert np.abs(fast - want).max() <= FLOAT_TOL * vrange(x)
+
+
+def test_config_c2_full(ctx, oracle_lib):
+    from paper_2108_05021_b200 import synth
+
+    cfg = synth.CONFIGS["C2"]
+    x = synth.make_input("C2")
+    want = np.stack([oracle_lib.osbf(c, cfg.radius, cfg.iterations, threads=8) for c in x])
+    exact = ctx.iterate(torch_dev(x), cfg.radius, cfg.iterations, mode="exact").cpu().numpy()
+    assert np.array_equal(bits(exact), bits(want))
+    fast = ctx.iterate(torch_dev(x), cfg.radius, cfg.iterations, mode="fast").cpu().numpy()
+    assert np.abs(fast - want).max() <= FLOAT_TOL * vrange(x)
+
+
+@pytest.mark.parametrize("r", [1, 2, 4, 8, 16])
+def test_config_c3_u8_radius_sweep(ctx, oracle_lib, r):
+    """C3 (uint8) at 1024x1024, 10 iterations: exact mode bit-exact at every
+    radius; fast mode bit-exact on the first pass (integer sums)."""
+    from paper_2108_05021_b200 import synth
+
+    x = synth.make_input("C3", shrink=4)[0]
+    want = oracle_lib.osbf(x, r, 10, threads=8)
+    got = ctx.iterate(torch_dev(x), r, 10, mode="exact").cpu().numpy()
+    assert np.array_equal(bits(got), bits(want))
+    one_fast = ctx.iterate(torch_dev(x), r, 1, mode="fast").cpu().numpy()
+    assert np.array_equal(bits(one_fast), bits(oracle_lib.osbf(x, r, 1)))
+
+
+@pytest.mark.parametrize("r", [1, 4, 16])
+def test_config_c3_full_first_pass(ctx, oracle_lib, r):
+    """Full 4096x4096 uint8: both modes bit-exact on the first pass."""
+    from paper_2108_05021_b200 import synth
+
+    x = synth.make_input("C3")[0]
+    want = oracle_lib.osbf(x, r, 1, threads=8)
+    for mode in ("exact", "fast"):
+        got = ctx.iterate(torch_dev(x), r, 1, mode=mode).cpu().numpy()
+        assert np.array_equal(bits(got), bits(want)), mode
+
+
+def test_batch_equals_individual_planes(ctx):
+    """C4-style batch: each plane is filtered independently (bit-identical)."""
+    from paper_2108_05021_b200 import synth
+
+    x = synth.make_input("C4", shrink=8)  # 32 x 128 x 128
+    for mode in ("exact", "fast"):
+        batched = ctx.iterate(torch_dev(x), 2, 4, mode=mode).cpu().numpy()
+        for i in (0, 1, 17, 31):
+            single = ctx.iterate(torch_dev(x[i]), 2, 4, mode=mode).cpu().numpy()
+            assert np.array_equal(bits(batched[i]), bits(single))
+
+
+def test_properties_at_full_size(ctx):
+    """Size-independent properties on a large plane: range preservation,
+    determinism, constant-plane and step fixed points, exact ~ fast."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    h, w = 4096, 8192
+    x = torch.from_numpy(rng.random((h, w), dtype=np.float64)).cuda()
+    for mode in ("exact", "fast"):
+        a = ctx.iterate(x, 4, 2, mode=mode)
+        b = ctx.iterate(x, 4, 2, mode=mode)
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64)), "not deterministic"
+        assert float(a.min()) >= float(x.min()) and float(a.max()) <= float(x.max())
+    e = ctx.iterate(x, 4, 2, mode="exact")
+    f = ctx.iterate(x, 4, 2, mode="fast")
+    assert float((e - f).abs().max()) <= FLOAT_TOL
+    c = torch.full((h, w), 3.5, dtype=torch.float64, device="cuda")
+    assert torch.equal(ctx.iterate(c, 16, 3, mode="exact"), c)
+    assert torch.equal(ctx.iterate(c, 16, 3, mode="fast"), c)
+    s = torch.where(torch.arange(w, device="cuda")[None, :] < w // 2, 0.0, 100.0).expand(h, w)
+    s = s.to(torch.float64).contiguous()
+    for mode in ("exact", "fast"):
+        assert torch.equal(ctx.iterate(s, 8, 5, mode=mode), s)
+
+
+def test_in_place_and_pitched(ctx, oracle_lib):
+    import torch
+
+    rng = np.random.default_rng(9)
+    p = rng.random((64, 96)) * 10
+    want = oracle_lib.osbf(p, 3, 3)
+    t = torch_dev(p)
+    ctx.iterate(t, 3, 3, mode="exact", out=t)  # in place
+    assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+    big = torch.zeros((64, 128), dtype=torch.float64, device="cuda")
+    big[:, :96] = torch_dev(p)
+    view = big[:, :96]  # pitched input (row stride 128)
+    got = ctx.iterate(view, 3, 3, mode="exact")
+    assert np.array_equal(bits(got.cpu().numpy()), bits(want))
