@@ -90,8 +90,8 @@ uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx);
  *   d_in  : device pointer, dtype `in_dtype`, batch x height x in_pitch
  *   d_out : device pointer, fp64, batch x height x out_pitch (may alias d_in
  *           only when in_dtype == OSBF_F64 and the pitches/strides match)
- *   stream: cudaStream_t (NULL = the context's stream); the call is
- *           asynchronous with respect to the host.
+ *   stream: cudaStream_t (NULL = the CUDA default stream, as everywhere in
+ *           CUDA); the call is asynchronous with respect to the host.
  * Errors (reference behaviour): iterations < 0 -> INVALID_ARGUMENT
  * (filters2d.hpp:92-93); radius < 1 with iterations > 0 -> INVALID_ARGUMENT
  * (filters2d.hpp:62-63); iterations == 0 copies without checking radius

@@ -117,9 +117,10 @@ osbf_status check_mode(osbf_mode m) {
     return OSBF_OK;
 }
 
-cudaStream_t pick_stream(osbf_ctx* ctx, void* stream) {
-    return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-}
+// NULL is the CUDA default stream (standard cudaStream_t semantics), so work
+// is ordered with e.g. PyTorch's default stream.  The context's own stream is
+// used only by the host-buffer entry points.
+cudaStream_t pick_stream(osbf_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
 // One pass in the requested mode: src (typed view) -> dst (fp64).
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
