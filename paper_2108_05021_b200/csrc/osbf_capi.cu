@@ -138,6 +138,10 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
                                          s, ctx->lc),
                   "exact select");
     } else {
+        if (r > osbf_gpu::kFastMaxRadius)
+            return fail(OSBF_ERR_INVALID_ARGUMENT,
+                        "fast mode supports radius <= %d (got %d); use OSBF_MODE_EXACT",
+                        osbf_gpu::kFastMaxRadius, r);
         OSBF_CUDA(osbf_gpu::fast_step(src, g, r, dst, dp, dpl, means, sel, s, ctx->lc),
                   "fast step");
     }

@@ -1,0 +1,330 @@
+// Fast-mode kernel templates (see osbf_fast.cu for the design notes).
+#pragma once
+// Fast mode: one OSBF pass with tile-local fp64 box sums.
+//
+// Each CTA owns a TW x TH output tile.  It stages the tile plus an R-pixel
+// halo in shared memory (zero outside the image, so clipped window sums need
+// no special casing; only the valid counts do, integral.hpp:53-61) and
+// evaluates the eight one-sided windows of the reference (core.hpp:212-225)
+// separably, in two phases:
+//
+//   Phase A (thread per tile row, walking x):  H(x,j) = sum_{u=-R..0} U(x+u, j)
+//            the "left arm" of every row; H(x+R, j) is the right arm.
+//   Phase B (thread per output column, walking y) keeps running vertical sums
+//            of three fields, F1 = H(x,.), F2 = H(x+R,.), F3 = U(x,.):
+//              Up(F) = sum over rows [y-R, y],  Dn(F) = sum over rows [y, y+R]
+//            and forms the eight windows
+//              w1 = Dn(F1)  w2 = Dn(F2)  w3 = Up(F2)  w4 = Up(F1)
+//              w5 = Up(F1)+Dn(F1)-F1(y)   w6 = Up(F2)+Dn(F2)-F2(y)
+//              w7 = Dn(F1)+Dn(F2)-Dn(F3)  w8 = Up(F1)+Up(F2)-Up(F3)
+//            then the valid-count means (integral.hpp:64-69), |a - u| and the
+//            strict-< first-minimum selection (filters2d.hpp:72-82).  Lanes
+//            are consecutive columns, so the output stores are coalesced.
+//
+// The radius is a template parameter (1..kFastMaxRadius): every shared-memory
+// offset is an immediate and the walks are fully unrolled, so values loaded
+// once stay in registers for the whole window (a register "ring" for free).
+// Interior tiles (no clipping anywhere) run a body with constant window counts;
+// border tiles run a body with per-pixel valid counts.  Work per pixel is O(1)
+// in R; sums never touch a whole-image prefix.
+//
+// Numerics: fp64 throughout.  Float input: selection on d_i = S_i/n_i - u
+// computed as fma(S_i, 1/n_i, -u), output u + d_m (a few ulps from the
+// reference's a_m; the tolerance is checked in tests).  uint8 input
+// (EXACT_DIV): sums are exact integers in any order, a_i = S_i/n_i is IEEE,
+// d_i = |a_i - u| and the output is a_m -> bit-identical to the reference.
+#include "osbf_internal.cuh"
+
+namespace osbf_gpu {
+namespace fastk {
+
+constexpr int TW = 64;   // output tile width  (Phase B: one thread column each)
+constexpr int TH = 64;   // output tile height
+constexpr int NT = 256;  // threads per CTA
+constexpr int NSB = NT / TW;    // Phase B row segments per column
+constexpr int SEGB = TH / NSB;  // rows per Phase B segment
+constexpr int kUnrollRadius = 4;  // full unroll (register ring) up to this radius
+
+template <int R>
+struct Lay {
+    static constexpr int LH = TH + 2 * R;      // staged rows
+    static constexpr int LWU = TW + 2 * R;     // staged columns of U
+    static constexpr int PU = LWU | 1;         // odd pitch: conflict-free row walks
+    static constexpr int LWH = TW + R;         // columns of H: H(X0 + k), k < LWH
+    static constexpr int PH = LWH | 1;
+    static constexpr int PER_ROW = (NT / LH) > 0 ? (NT / LH) : 1;  // Phase A threads per row
+    static constexpr int SEGA = (LWH + PER_ROW - 1) / PER_ROW;     // Phase A walk length
+    static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(LH) * (PU + PH);
+};
+
+__device__ __forceinline__ void cp_async_f64(double* dst, const double* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int n = valid ? 8 : 0;  // src-size 0 -> zero fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Stage U rows [Y0-R, Y0+TH+R) x cols [X0-R, X0+TW+R), zero outside the image.
+template <int R, typename T, bool BORDER>
+__device__ __forceinline__ void stage_tile(const T* __restrict__ src, size_t pitch, int X0,
+                                           int Y0, int W, int H, double* __restrict__ Us) {
+    using Ly = Lay<R>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int CHUNKS = (Ly::LWU + 31) / 32;
+    for (int j = warp; j < Ly::LH; j += NT / 32) {
+        const int gy = Y0 - R + j;
+        const bool row_in = !BORDER || (gy >= 0 && gy < H);
+        const T* rowp = src + static_cast<size_t>(row_in ? gy : 0) * pitch;
+#pragma unroll
+        for (int c = 0; c < CHUNKS; ++c) {
+            const int i = lane + 32 * c;
+            if (i < Ly::LWU) {
+                const int gx = X0 - R + i;
+                const bool ok = row_in && (!BORDER || (gx >= 0 && gx < W));
+                if constexpr (sizeof(T) == 8) {
+                    cp_async_f64(Us + j * Ly::PU + i,
+                                 reinterpret_cast<const double*>(rowp) + (ok ? gx : 0), ok);
+                } else {
+                    Us[j * Ly::PU + i] = ok ? to_f64(rowp[gx]) : 0.0;
+                }
+            }
+        }
+    }
+    if constexpr (sizeof(T) == 8) cp_async_wait_all();
+}
+
+// Phase A: Hs[j][k] = sum_{i=k}^{k+R} Us[j][i] for k < LWH (lanes = rows).
+template <int R>
+__device__ __forceinline__ void arm_sums(const double* __restrict__ Us, double* __restrict__ Hs) {
+    using Ly = Lay<R>;
+    const int tid = threadIdx.x;
+    const int j = tid % Ly::LH, s = tid / Ly::LH;
+    if (s >= Ly::PER_ROW) return;
+    const int k0 = s * Ly::SEGA;
+    const double* __restrict__ u = Us + j * Ly::PU + k0;
+    double* __restrict__ h = Hs + j * Ly::PH + k0;
+    if (k0 + Ly::SEGA <= Ly::LWH) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i <= R; ++i) acc += u[i];
+        h[0] = acc;
+#pragma unroll(R <= kUnrollRadius ? Ly::SEGA : 4)
+        for (int k = 1; k < Ly::SEGA; ++k) {
+            acc += u[k + R] - u[k - 1];
+            h[k] = acc;
+        }
+    } else {  // last, shorter segment
+        const int n = Ly::LWH - k0;
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i <= R; ++i) acc += u[i];
+        h[0] = acc;
+        for (int k = 1; k < n; ++k) {
+            acc += u[k + R] - u[k - 1];
+            h[k] = acc;
+        }
+    }
+}
+
+// Per-window valid counts at (gx, gy) (integral.hpp:53-61, clipped ranges).
+struct Counts {
+    int n[8];
+};
+template <int R>
+__device__ __forceinline__ Counts border_counts(int gx, int gy, int W, int H) {
+    const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+    const int nru = min(gy, R) + 1, nrd = min(H - 1 - gy, R) + 1;
+    Counts c;
+    c.n[0] = ncl * nrd;
+    c.n[1] = ncr * nrd;
+    c.n[2] = ncr * nru;
+    c.n[3] = ncl * nru;
+    c.n[4] = ncl * (nru + nrd - 1);
+    c.n[5] = ncr * (nru + nrd - 1);
+    c.n[6] = (ncl + ncr - 1) * nrd;
+    c.n[7] = (ncl + ncr - 1) * nru;
+    return c;
+}
+
+// Phase B for one thread: output column x, rows [y0, y0 + SEGB) of the tile.
+template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
+__device__ __forceinline__ void column_walk(const double* __restrict__ Us,
+                                            const double* __restrict__ Hs, int X0, int Y0,
+                                            int W, int H, int b, double* __restrict__ outp,
+                                            size_t out_pitch, double* __restrict__ means,
+                                            uint8_t* __restrict__ sel) {
+    using Ly = Lay<R>;
+    const int x = threadIdx.x % TW, s = threadIdx.x / TW;
+    const int gx = X0 + x;
+    if (BORDER && gx >= W) return;
+    const int y0 = s * SEGB;
+    const double* f1 = Hs + y0 * Ly::PH + x;      // F1(j) = f1[j*PH]
+    const double* f2 = Hs + y0 * Ly::PH + x + R;  // F2(j)
+    const double* f3 = Us + y0 * Ly::PU + x + R;  // F3(j)
+#define F1(j) f1[(j) * Ly::PH]
+#define F2(j) f2[(j) * Ly::PH]
+#define F3(j) f3[(j) * Ly::PU]
+    // Up(y) = sum_{j=y}^{y+R} F(j), Dn(y) = sum_{j=y+R}^{y+2R} F(j) (rows relative to y0)
+    double up1 = 0.0, up2 = 0.0, up3 = 0.0, dn1 = 0.0, dn2 = 0.0, dn3 = 0.0;
+#pragma unroll
+    for (int j = 0; j <= R; ++j) {
+        up1 += F1(j);
+        up2 += F2(j);
+        up3 += F3(j);
+        dn1 += F1(j + R);
+        dn2 += F2(j + R);
+        dn3 += F3(j + R);
+    }
+    constexpr double kRq = 1.0 / ((R + 1) * (R + 1));
+    constexpr double kRh = 1.0 / ((R + 1) * (2 * R + 1));
+    constexpr int kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
+    double* __restrict__ o = outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx;
+    // Small radii: fully unrolled, every F value is loaded once and stays in a
+    // register for its whole window.  Larger radii: rolled loop (register
+    // pressure), pointers advance one row per step, offsets are immediates.
+    double c1 = F1(R), c2 = F2(R), u = F3(R);
+#pragma unroll(R <= kUnrollRadius ? SEGB : 1)
+    for (int y = 0; y < SEGB; ++y) {
+        if (y > 0) {
+            const double n1 = F1(R), n2 = F2(R), n3 = F3(R);  // pointers already advanced
+            up1 += n1 - F1(-1);
+            up2 += n2 - F2(-1);
+            up3 += n3 - F3(-1);
+            dn1 += F1(2 * R) - c1;
+            dn2 += F2(2 * R) - c2;
+            dn3 += F3(2 * R) - u;
+            c1 = n1;
+            c2 = n2;
+            u = n3;
+        }
+        const int gy = Y0 + y0 + y;
+        if (BORDER && gy >= H) break;
+        const double S[8] = {dn1, dn2, up2, up1, up1 + dn1 - c1, up2 + dn2 - c2,
+                             dn1 + dn2 - dn3, up1 + up2 - up3};
+        Counts cn;
+        if (BORDER) {
+            cn = border_counts<R>(gx, gy, W, H);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cn.n[i] = i < 4 ? kNq : kNh;
+        }
+        double result;
+        int best_id = 0;
+        if (EXACT_DIV || DIAG) {
+            // Reference arithmetic: a_i = S_i / n_i (IEEE), d_i = |a_i - u|, strict <.
+            double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
+            const size_t pix = (static_cast<size_t>(b) * H + gy) * W + gx;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double a = EXACT_DIV ? __ddiv_rn(S[i], static_cast<double>(cn.n[i]))
+                                           : S[i] * (BORDER ? 1.0 / cn.n[i] : (i < 4 ? kRq : kRh));
+                if (DIAG && means) means[pix * 8 + i] = a;
+                const double d = fabs(a - u);
+                if (d < best_abs) {
+                    best_abs = d;
+                    best = a;
+                    best_id = i + 1;
+                }
+            }
+            if (DIAG && sel) sel[pix] = static_cast<uint8_t>(best_id);
+            result = best;
+        } else {
+            // d_i = S_i * (1/n_i) - u in one rounding; first |d| minimum wins.
+            double best_d = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double rc = BORDER ? __drcp_rn(static_cast<double>(cn.n[i]))
+                                         : (i < 4 ? kRq : kRh);
+                const double d = fma(S[i], rc, -u);
+                if (fabs(d) < fabs(best_d)) best_d = d;
+            }
+            result = fabs(best_d) < __longlong_as_double(0x7ff0000000000000LL) ? u + best_d : 0.0;
+        }
+        if (outp) o[static_cast<size_t>(y) * out_pitch] = result;
+        f1 += Ly::PH;
+        f2 += Ly::PH;
+        f3 += Ly::PU;
+    }
+#undef F1
+#undef F2
+#undef F3
+}
+
+template <int R, typename T, bool EXACT_DIV, bool DIAG>
+__global__ void __launch_bounds__(NT, 2)
+    fast_sep_step(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
+                  double* __restrict__ out, size_t out_pitch, size_t out_plane,
+                  double* __restrict__ means, uint8_t* __restrict__ sel, int W, int H) {
+    extern __shared__ double smem[];
+    using Ly = Lay<R>;
+    double* Us = smem;                   // [LH][PU]: tile row j <-> image row Y0 - R + j
+    double* Hs = smem + Ly::LH * Ly::PU;  // [LH][PH]: Hs[j][k] = H(X0 + k, row j)
+    const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH, b = blockIdx.z;
+    const T* src = in + static_cast<size_t>(b) * in_plane;
+    double* outp = out ? out + static_cast<size_t>(b) * out_plane : nullptr;
+    const bool interior = X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= H;
+    if (interior) {
+        stage_tile<R, T, false>(src, in_pitch, X0, Y0, W, H, Us);
+    } else {
+        stage_tile<R, T, true>(src, in_pitch, X0, Y0, W, H, Us);
+    }
+    __syncthreads();
+    arm_sums<R>(Us, Hs);
+    __syncthreads();
+    if (interior) {
+        column_walk<R, EXACT_DIV, false, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
+                                               sel);
+    } else {
+        column_walk<R, EXACT_DIV, true, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
+                                              sel);
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV, bool DIAG>
+cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t op, size_t opl,
+                     double* means, uint8_t* sel, cudaStream_t s) {
+    constexpr size_t smem = Lay<R>::SMEM;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_sep_step<R, T, EXACT_DIV, DIAG>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    fast_sep_step<R, T, EXACT_DIV, DIAG><<<grid, NT, smem, s>>>(
+        static_cast<const T*>(in.base), in.pitch, in.plane, out, op, opl, means, sel, g.width,
+        g.height);
+    return cudaGetLastError();
+}
+
+template <int R, bool DIAG>
+cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                         size_t opl, double* means, uint8_t* sel, cudaStream_t s) {
+    switch (in.dtype) {
+        case OSBF_U8:
+            return launch_r<R, uint8_t, true, DIAG>(in, g, out, op, opl, means, sel, s);
+        case OSBF_F32:
+            return launch_r<R, float, false, DIAG>(in, g, out, op, opl, means, sel, s);
+        default:
+            return launch_r<R, double, false, DIAG>(in, g, out, op, opl, means, sel, s);
+    }
+}
+
+}  // namespace fastk
+
+// One radius: all dtypes and the diagnostic variant (explicitly instantiated
+// in osbf_fast_rNN.cu so the radii compile in parallel).
+template <int R>
+cudaError_t fast_launch_radius(const PlaneView& in, const Geometry& g, double* out,
+                               size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
+                               cudaStream_t s) {
+    if (means || sel)
+        return fastk::launch_dtype<R, true>(in, g, out, out_pitch, out_plane, means, sel, s);
+    return fastk::launch_dtype<R, false>(in, g, out, out_pitch, out_plane, means, sel, s);
+}
+
+}  // namespace osbf_gpu

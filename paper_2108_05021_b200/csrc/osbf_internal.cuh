@@ -44,6 +44,8 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
                          uint8_t* sel, cudaStream_t s, LaunchCounter& lc);
 
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
+// Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
+constexpr int kFastMaxRadius = 16;
 // One OSBF pass with tile-local fp64 summed-area tables.
 cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double* out,
                       size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
