@@ -54,7 +54,8 @@ struct Lay {
     static constexpr int PH = LWH | 1;
     static constexpr int PER_ROW = (NT / LH) > 0 ? (NT / LH) : 1;  // Phase A threads per row
     static constexpr int SEGA = (LWH + PER_ROW - 1) / PER_ROW;     // Phase A walk length
-    static constexpr size_t SMEM = sizeof(double) * static_cast<size_t>(LH) * (PU + PH);
+    static constexpr int NRT = 2 * R + 2;      // reciprocal table 1/k, k < NRT
+    static constexpr size_t SMEM = sizeof(double) * (static_cast<size_t>(LH) * (PU + PH) + NRT);
 };
 
 __device__ __forceinline__ void cp_async_f64(double* dst, const double* src, bool valid) {
@@ -154,11 +155,16 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
                                             const double* __restrict__ Hs, int X0, int Y0,
                                             int W, int H, int b, double* __restrict__ outp,
                                             size_t out_pitch, double* __restrict__ means,
-                                            uint8_t* __restrict__ sel) {
+                                            uint8_t* __restrict__ sel,
+                                            const double* __restrict__ rtab) {
     using Ly = Lay<R>;
     const int x = threadIdx.x % TW, s = threadIdx.x / TW;
     const int gx = X0 + x;
     if (BORDER && gx >= W) return;
+    // column factors of the valid counts (border tiles only)
+    const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+    const double cL = BORDER ? rtab[ncl] : 0.0, cR = BORDER ? rtab[ncr] : 0.0,
+                 cF = BORDER ? rtab[ncl + ncr - 1] : 0.0;
     const int y0 = s * SEGB;
     const double* f1 = Hs + y0 * Ly::PH + x;      // F1(j) = f1[j*PH]
     const double* f2 = Hs + y0 * Ly::PH + x + R;  // F2(j)
@@ -203,18 +209,18 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
         if (BORDER && gy >= H) break;
         const double S[8] = {dn1, dn2, up2, up1, up1 + dn1 - c1, up2 + dn2 - c2,
                              dn1 + dn2 - dn3, up1 + up2 - up3};
-        Counts cn;
-        if (BORDER) {
-            cn = border_counts<R>(gx, gy, W, H);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) cn.n[i] = i < 4 ? kNq : kNh;
-        }
         double result;
-        int best_id = 0;
         if (EXACT_DIV || DIAG) {
             // Reference arithmetic: a_i = S_i / n_i (IEEE), d_i = |a_i - u|, strict <.
+            Counts cn;
+            if (BORDER) {
+                cn = border_counts<R>(gx, gy, W, H);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cn.n[i] = i < 4 ? kNq : kNh;
+            }
             double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
+            int best_id = 0;
             const size_t pix = (static_cast<size_t>(b) * H + gy) * W + gx;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -231,18 +237,33 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
             if (DIAG && sel) sel[pix] = static_cast<uint8_t>(best_id);
             result = best;
         } else {
-            // d_i = S_i * (1/n_i) - u in one rounding; first |d| minimum wins.
-            double best_d = __longlong_as_double(0x7ff0000000000000LL);
+            // 1/n_i: interior constants, or products of clipped row/column
+            // factors 1/n_row * 1/n_col from the per-CTA table (border tiles).
+            double rc[8];
+            if (BORDER) {
+                const int nru = min(gy, R) + 1, nrd = min(H - 1 - gy, R) + 1;
+                const double rU = rtab[nru], rD = rtab[nrd], rF = rtab[nru + nrd - 1];
+                rc[0] = cL * rD; rc[1] = cR * rD; rc[2] = cR * rU; rc[3] = cL * rU;
+                rc[4] = cL * rF; rc[5] = cR * rF; rc[6] = cF * rD; rc[7] = cF * rU;
+            } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double rc = BORDER ? __drcp_rn(static_cast<double>(cn.n[i]))
-                                         : (i < 4 ? kRq : kRh);
-                const double d = fma(S[i], rc, -u);
-                if (fabs(d) < fabs(best_d)) best_d = d;
+                for (int i = 0; i < 8; ++i) rc[i] = i < 4 ? kRq : kRh;
             }
-            result = fabs(best_d) < __longlong_as_double(0x7ff0000000000000LL) ? u + best_d : 0.0;
+            // d_i = S_i/n_i - u in one rounding; stable tournament keeps the
+            // first minimum of |d_i| (filters2d.hpp:78 strict <) at depth 3.
+            double d[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = fma(S[i], rc[i], -u);
+            auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
+            const double best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
+                                     pick(pick(d[4], d[5]), pick(d[6], d[7])));
+            result = fabs(best) < __longlong_as_double(0x7ff0000000000000LL) ? u + best : 0.0;
         }
-        if (outp) o[static_cast<size_t>(y) * out_pitch] = result;
+        if (DIAG) {
+            if (outp) o[static_cast<size_t>(y) * out_pitch] = result;
+        } else {
+            o[static_cast<size_t>(y) * out_pitch] = result;
+        }
         f1 += Ly::PH;
         f2 += Ly::PH;
         f3 += Ly::PU;
@@ -264,6 +285,8 @@ __global__ void __launch_bounds__(NT, 2)
     const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH, b = blockIdx.z;
     const T* src = in + static_cast<size_t>(b) * in_plane;
     double* outp = out ? out + static_cast<size_t>(b) * out_plane : nullptr;
+    double* rtab = Hs + Ly::LH * Ly::PH;  // [NRT]: rtab[k] = 1/k
+    if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
     const bool interior = X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= H;
     if (interior) {
         stage_tile<R, T, false>(src, in_pitch, X0, Y0, W, H, Us);
@@ -275,10 +298,10 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
     if (interior) {
         column_walk<R, EXACT_DIV, false, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
-                                               sel);
+                                               sel, rtab);
     } else {
         column_walk<R, EXACT_DIV, true, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
-                                              sel);
+                                              sel, rtab);
     }
 }
 
