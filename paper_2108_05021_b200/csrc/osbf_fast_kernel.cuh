@@ -10,8 +10,8 @@
 //
 //   Phase A (thread per tile row, walking x):  H(x,j) = sum_{u=-R..0} U(x+u, j)
 //            the "left arm" of every row; H(x+R, j) is the right arm.
-//   Phase B (thread per output column, walking y) keeps running vertical sums
-//            of three fields, F1 = H(x,.), F2 = H(x+R,.), F3 = U(x,.):
+//   Phase B (thread per output column, walking y) combines vertical sums of
+//            three fields, F1 = H(x,.), F2 = H(x+R,.), F3 = U(x,.):
 //              Up(F) = sum over rows [y-R, y],  Dn(F) = sum over rows [y, y+R]
 //            and forms the eight windows
 //              w1 = Dn(F1)  w2 = Dn(F2)  w3 = Up(F2)  w4 = Up(F1)
@@ -22,8 +22,8 @@
 //            are consecutive columns, so the output stores are coalesced.
 //
 // The radius is a template parameter (1..kFastMaxRadius): every shared-memory
-// offset is an immediate and the walks are fully unrolled, so values loaded
-// once stay in registers for the whole window (a register "ring" for free).
+// offset is an immediate; for small radii the walks are fully unrolled, so
+// values loaded once stay in registers for their whole window.
 // Interior tiles (no clipping anywhere) run a body with constant window counts;
 // border tiles run a body with per-pixel valid counts.  Work per pixel is O(1)
 // in R; sums never touch a whole-image prefix.
@@ -56,6 +56,12 @@ struct Lay {
     static constexpr int SEGA = (LWH + PER_ROW - 1) / PER_ROW;     // Phase A walk length
     static constexpr int NRT = 2 * R + 2;      // reciprocal table 1/k, k < NRT
     static constexpr size_t SMEM = sizeof(double) * (static_cast<size_t>(LH) * (PU + PH) + NRT);
+    // 3 CTAs/SM when shared memory (incl. the 1 KB driver reserve per CTA)
+    // allows it; the register budget then caps at 80/thread.
+    template <bool SLOW>
+    static constexpr int min_ctas() {
+        return (!SLOW && (SMEM + 1024) * 3 <= 228 * 1024) ? 3 : 2;
+    }
 };
 
 __device__ __forceinline__ void cp_async_f64(double* dst, const double* src, bool valid) {
@@ -149,7 +155,85 @@ __device__ __forceinline__ Counts border_counts(int gx, int gy, int W, int H) {
     return c;
 }
 
+// Valid-count factors of one column (border tiles): 1/ncl, 1/ncr, 1/(ncl+ncr-1).
+struct ColFactors {
+    double cL, cR, cF;
+};
+
+// Means, |a-u| selection and the store for one pixel (S = the eight window
+// sums in reference order, u = the centre sample).
+template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
+__device__ __forceinline__ void select_store(const double (&S)[8], double u, int gx, int gy,
+                                             int W, int H, int b, double* __restrict__ o,
+                                             double* __restrict__ means,
+                                             uint8_t* __restrict__ sel, const ColFactors& cf,
+                                             const double* __restrict__ rtab) {
+    constexpr double kRq = 1.0 / ((R + 1) * (R + 1));
+    constexpr double kRh = 1.0 / ((R + 1) * (2 * R + 1));
+    constexpr int kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
+    if (EXACT_DIV || DIAG) {
+        // Reference arithmetic: a_i = S_i / n_i (IEEE), d_i = |a_i - u|,
+        // strict < in window order, output a_m (filters2d.hpp:74-83).
+        Counts cn;
+        if (BORDER) {
+            cn = border_counts<R>(gx, gy, W, H);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cn.n[i] = i < 4 ? kNq : kNh;
+        }
+        double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
+        int best_id = 0;
+        const size_t pix = (static_cast<size_t>(b) * H + gy) * W + gx;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double a = EXACT_DIV ? __ddiv_rn(S[i], static_cast<double>(cn.n[i]))
+                                       : S[i] * (BORDER ? 1.0 / cn.n[i] : (i < 4 ? kRq : kRh));
+            if (DIAG && means) means[pix * 8 + i] = a;
+            const double d = fabs(a - u);
+            if (d < best_abs) {
+                best_abs = d;
+                best = a;
+                best_id = i + 1;
+            }
+        }
+        if (DIAG && sel) sel[pix] = static_cast<uint8_t>(best_id);
+        if (!DIAG || o) *o = best;
+        return;
+    }
+    // 1/n_i: interior constants, or products of clipped row/column factors
+    // 1/n_row * 1/n_col from the per-CTA table (border tiles).
+    double rc[8];
+    if (BORDER) {
+        const int nru = min(gy, R) + 1, nrd = min(H - 1 - gy, R) + 1;
+        const double rU = rtab[nru], rD = rtab[nrd], rF = rtab[nru + nrd - 1];
+        rc[0] = cf.cL * rD; rc[1] = cf.cR * rD; rc[2] = cf.cR * rU; rc[3] = cf.cL * rU;
+        rc[4] = cf.cL * rF; rc[5] = cf.cR * rF; rc[6] = cf.cF * rD; rc[7] = cf.cF * rU;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rc[i] = i < 4 ? kRq : kRh;
+    }
+    // d_i = S_i/n_i - u in one rounding; a stable tournament keeps the first
+    // minimum of |d_i| (filters2d.hpp:78 strict <) at depth 3.  Finite input
+    // assumed (non-finite samples: use exact mode).
+    double d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = fma(S[i], rc[i], -u);
+    auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
+    const double best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
+                             pick(pick(d[4], d[5]), pick(d[6], d[7])));
+    *o = u + best;
+}
+
 // Phase B for one thread: output column x, rows [y0, y0 + SEGB) of the tile.
+//
+// Small radii (R <= kUnrollRadius): fully unrolled over column prefix sums
+//   P1(j) = sum_{j'<=j} F1, P2 likewise, Q(j) = sum (F1 + F2 - F3), so that
+//   w4 = P1(y+R)-P1(y-1)   w1 = P1(y+2R)-P1(y+R-1)   w5 = P1(y+2R)-P1(y-1)
+//   w3 = P2(y+R)-P2(y-1)   w2 = P2(y+2R)-P2(y+R-1)   w6 = P2(y+2R)-P2(y-1)
+//   w8 = Q(y+R)-Q(y-1)     w7 = Q(y+2R)-Q(y+R-1)
+//   (one subtraction per window; every value stays in registers).
+// Larger radii: rolled loop with running Up/Dn sums (register pressure),
+//   pointers advance one row per step, every offset is an immediate.
 template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
 __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
                                             const double* __restrict__ Hs, int X0, int Y0,
@@ -161,112 +245,81 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
     const int x = threadIdx.x % TW, s = threadIdx.x / TW;
     const int gx = X0 + x;
     if (BORDER && gx >= W) return;
-    // column factors of the valid counts (border tiles only)
-    const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
-    const double cL = BORDER ? rtab[ncl] : 0.0, cR = BORDER ? rtab[ncr] : 0.0,
-                 cF = BORDER ? rtab[ncl + ncr - 1] : 0.0;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (BORDER) {
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
     const int y0 = s * SEGB;
     const double* f1 = Hs + y0 * Ly::PH + x;      // F1(j) = f1[j*PH]
     const double* f2 = Hs + y0 * Ly::PH + x + R;  // F2(j)
     const double* f3 = Us + y0 * Ly::PU + x + R;  // F3(j)
+    double* o = outp ? outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx : nullptr;
 #define F1(j) f1[(j) * Ly::PH]
 #define F2(j) f2[(j) * Ly::PH]
 #define F3(j) f3[(j) * Ly::PU]
-    // Up(y) = sum_{j=y}^{y+R} F(j), Dn(y) = sum_{j=y+R}^{y+2R} F(j) (rows relative to y0)
-    double up1 = 0.0, up2 = 0.0, up3 = 0.0, dn1 = 0.0, dn2 = 0.0, dn3 = 0.0;
+    if constexpr (R <= kUnrollRadius) {
+        constexpr int NJ = SEGB + 2 * R;  // rows touched by this segment
+        double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
+        P1[0] = P2[0] = Q[0] = 0.0;  // P(j) lives at index j + 1
 #pragma unroll
-    for (int j = 0; j <= R; ++j) {
-        up1 += F1(j);
-        up2 += F2(j);
-        up3 += F3(j);
-        dn1 += F1(j + R);
-        dn2 += F2(j + R);
-        dn3 += F3(j + R);
-    }
-    constexpr double kRq = 1.0 / ((R + 1) * (R + 1));
-    constexpr double kRh = 1.0 / ((R + 1) * (2 * R + 1));
-    constexpr int kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
-    double* __restrict__ o = outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx;
-    // Small radii: fully unrolled, every F value is loaded once and stays in a
-    // register for its whole window.  Larger radii: rolled loop (register
-    // pressure), pointers advance one row per step, offsets are immediates.
-    double c1 = F1(R), c2 = F2(R), u = F3(R);
-#pragma unroll(R <= kUnrollRadius ? SEGB : 1)
-    for (int y = 0; y < SEGB; ++y) {
-        if (y > 0) {
-            const double n1 = F1(R), n2 = F2(R), n3 = F3(R);  // pointers already advanced
-            up1 += n1 - F1(-1);
-            up2 += n2 - F2(-1);
-            up3 += n3 - F3(-1);
-            dn1 += F1(2 * R) - c1;
-            dn2 += F2(2 * R) - c2;
-            dn3 += F3(2 * R) - u;
-            c1 = n1;
-            c2 = n2;
-            u = n3;
-        }
-        const int gy = Y0 + y0 + y;
-        if (BORDER && gy >= H) break;
-        const double S[8] = {dn1, dn2, up2, up1, up1 + dn1 - c1, up2 + dn2 - c2,
-                             dn1 + dn2 - dn3, up1 + up2 - up3};
-        double result;
-        if (EXACT_DIV || DIAG) {
-            // Reference arithmetic: a_i = S_i / n_i (IEEE), d_i = |a_i - u|, strict <.
-            Counts cn;
-            if (BORDER) {
-                cn = border_counts<R>(gx, gy, W, H);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) cn.n[i] = i < 4 ? kNq : kNh;
+        for (int j = 0; j < NJ; ++j) {
+            const double a = F1(j), c = F2(j), e = F3(j);
+            Uc[j] = e;
+            P1[j + 1] = P1[j] + a;
+            P2[j + 1] = P2[j] + c;
+            Q[j + 1] = Q[j] + ((a + c) - e);
+            const int y = j - 2 * R;  // output row whose windows complete at row j
+            if (y >= 0) {
+                const int gy = Y0 + y0 + y;
+                if (BORDER && gy >= H) break;
+                const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                     P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                     P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                     Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+                select_store<R, EXACT_DIV, BORDER, DIAG>(
+                    S, Uc[y + R], gx, gy, W, H, b, o ? o + static_cast<size_t>(y) * out_pitch : o,
+                    means, sel, cf, rtab);
             }
-            double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
-            int best_id = 0;
-            const size_t pix = (static_cast<size_t>(b) * H + gy) * W + gx;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double a = EXACT_DIV ? __ddiv_rn(S[i], static_cast<double>(cn.n[i]))
-                                           : S[i] * (BORDER ? 1.0 / cn.n[i] : (i < 4 ? kRq : kRh));
-                if (DIAG && means) means[pix * 8 + i] = a;
-                const double d = fabs(a - u);
-                if (d < best_abs) {
-                    best_abs = d;
-                    best = a;
-                    best_id = i + 1;
-                }
-            }
-            if (DIAG && sel) sel[pix] = static_cast<uint8_t>(best_id);
-            result = best;
-        } else {
-            // 1/n_i: interior constants, or products of clipped row/column
-            // factors 1/n_row * 1/n_col from the per-CTA table (border tiles).
-            double rc[8];
-            if (BORDER) {
-                const int nru = min(gy, R) + 1, nrd = min(H - 1 - gy, R) + 1;
-                const double rU = rtab[nru], rD = rtab[nrd], rF = rtab[nru + nrd - 1];
-                rc[0] = cL * rD; rc[1] = cR * rD; rc[2] = cR * rU; rc[3] = cL * rU;
-                rc[4] = cL * rF; rc[5] = cR * rF; rc[6] = cF * rD; rc[7] = cF * rU;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) rc[i] = i < 4 ? kRq : kRh;
-            }
-            // d_i = S_i/n_i - u in one rounding; stable tournament keeps the
-            // first minimum of |d_i| (filters2d.hpp:78 strict <) at depth 3.
-            double d[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) d[i] = fma(S[i], rc[i], -u);
-            auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
-            const double best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
-                                     pick(pick(d[4], d[5]), pick(d[6], d[7])));
-            result = fabs(best) < __longlong_as_double(0x7ff0000000000000LL) ? u + best : 0.0;
         }
-        if (DIAG) {
-            if (outp) o[static_cast<size_t>(y) * out_pitch] = result;
-        } else {
-            o[static_cast<size_t>(y) * out_pitch] = result;
+    } else {
+        // Up(y) = sum_{j=y}^{y+R} F(j), Dn(y) = sum_{j=y+R}^{y+2R} F(j) (rows relative to y0)
+        double up1 = 0.0, up2 = 0.0, up3 = 0.0, dn1 = 0.0, dn2 = 0.0, dn3 = 0.0;
+#pragma unroll
+        for (int j = 0; j <= R; ++j) {
+            up1 += F1(j);
+            up2 += F2(j);
+            up3 += F3(j);
+            dn1 += F1(j + R);
+            dn2 += F2(j + R);
+            dn3 += F3(j + R);
         }
-        f1 += Ly::PH;
-        f2 += Ly::PH;
-        f3 += Ly::PU;
+        double c1 = F1(R), c2 = F2(R), u = F3(R);
+#pragma unroll 1
+        for (int y = 0; y < SEGB; ++y) {
+            if (y > 0) {
+                const double n1 = F1(R), n2 = F2(R), n3 = F3(R);  // pointers already advanced
+                up1 += n1 - F1(-1);
+                up2 += n2 - F2(-1);
+                up3 += n3 - F3(-1);
+                dn1 += F1(2 * R) - c1;
+                dn2 += F2(2 * R) - c2;
+                dn3 += F3(2 * R) - u;
+                c1 = n1;
+                c2 = n2;
+                u = n3;
+            }
+            const int gy = Y0 + y0 + y;
+            if (BORDER && gy >= H) break;
+            const double S[8] = {dn1, dn2, up2, up1, up1 + dn1 - c1, up2 + dn2 - c2,
+                                 dn1 + dn2 - dn3, up1 + up2 - up3};
+            select_store<R, EXACT_DIV, BORDER, DIAG>(
+                S, u, gx, gy, W, H, b, o ? o + static_cast<size_t>(y) * out_pitch : o, means, sel,
+                cf, rtab);
+            f1 += Ly::PH;
+            f2 += Ly::PH;
+            f3 += Ly::PU;
+        }
     }
 #undef F1
 #undef F2
@@ -274,7 +327,7 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
 }
 
 template <int R, typename T, bool EXACT_DIV, bool DIAG>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, Lay<R>::template min_ctas<EXACT_DIV || DIAG>())
     fast_sep_step(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
                   double* __restrict__ out, size_t out_pitch, size_t out_plane,
                   double* __restrict__ means, uint8_t* __restrict__ sel, int W, int H) {
