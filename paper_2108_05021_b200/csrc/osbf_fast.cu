@@ -1,8 +1,48 @@
 // Fast mode dispatch: radius -> compiled kernel (osbf_fast_rNN.cu).
 // Design notes and the kernel itself: osbf_fast_kernel.cuh.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "osbf_internal.cuh"
+#include "osbf_tma.cuh"
 
 namespace osbf_gpu {
+
+namespace tma {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+}  // namespace
+
+bool encode_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t width,
+               uint64_t height, uint64_t planes, uint64_t pitch_bytes, uint64_t plane_bytes,
+               uint32_t box_w, uint32_t box_h) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
+    if (pitch_bytes % 16 != 0 || plane_bytes % 16 != 0) return false;
+    if (box_w > 256 || box_h > 256) return false;
+    const cuuint64_t dims[3] = {width, height, planes};
+    const cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
+    const cuuint32_t box[3] = {box_w, box_h, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, dtype, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace tma
 
 template <int R>
 cudaError_t fast_launch_radius(const PlaneView& in, const Geometry& g, double* out,

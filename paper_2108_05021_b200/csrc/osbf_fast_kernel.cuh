@@ -34,6 +34,7 @@
 // (EXACT_DIV): sums are exact integers in any order, a_i = S_i/n_i is IEEE,
 // d_i = |a_i - u| and the output is a_m -> bit-identical to the reference.
 #include "osbf_internal.cuh"
+#include "osbf_tma.cuh"
 
 namespace osbf_gpu {
 namespace fastk {
@@ -377,9 +378,152 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Small radii (R <= kUnrollRadius): TMA-staged tile, no separate Phase A.
+//
+// One thread issues a single cp.async.bulk.tensor for the whole (TW+2R) x
+// (TH+2R) tile (hardware zero-fill outside the image); the column threads
+// then form F1 = sum Us[j][x..x+R], F2 = sum Us[j][x+R..x+2R] themselves
+// (2R+1 conflict-free loads per row, consecutive lanes = consecutive x) and
+// run the prefix-sum walk.  The input is read in its own dtype (u8 / f32 /
+// f64) and promoted to fp64 in registers, so the first pass needs no
+// conversion kernel.
+template <int R, typename T>
+struct TLay {
+    static constexpr int LH = TH + 2 * R;
+    static constexpr int LWU = TW + 2 * R;
+    // TMA needs 16-byte aligned box rows AND a 16-byte aligned innermost start
+    // coordinate, so the box starts RA >= R columns left of the tile
+    // (RA = R rounded up to 16 bytes) and column x of the tile sits at
+    // smem column x + XOFF.
+    static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
+    static constexpr int RA = (R + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int XOFF = RA - R;
+    static constexpr int BW = (TW + RA + R + ALIGN - 1) / ALIGN * ALIGN;  // TMA box width
+    static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
+    static constexpr int NRT = 2 * R + 2;
+    static constexpr size_t SMEM = TILE_BYTES + 128;  // + alignment slack
+};
+
+template <int R, typename T, bool EXACT_DIV, bool BORDER>
+__device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, int Y0, int W,
+                                            int H, int b, double* __restrict__ outp,
+                                            size_t out_pitch, const double* __restrict__ rtab) {
+    using Ly = TLay<R, T>;
+    const int x = threadIdx.x % TW, s = threadIdx.x / TW;
+    const int gx = X0 + x;
+    if (BORDER && gx >= W) return;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (BORDER) {
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    const int y0 = s * SEGB;
+    // image (X0 + x + i - R, Y0 + y0 + j - R) = col[j*BW + i]
+    const T* __restrict__ col = Us + y0 * Ly::BW + x + Ly::XOFF;
+    double* o = outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx;
+    constexpr int NJ = SEGB + 2 * R;
+    double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
+    P1[0] = P2[0] = Q[0] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        double v[2 * R + 1];
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) v[i] = to_f64(col[j * Ly::BW + i]);
+        double a = v[0], c = v[R];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) {
+            a += v[i];
+            c += v[R + i];
+        }
+        const double e = v[R];
+        Uc[j] = e;
+        P1[j + 1] = P1[j] + a;
+        P2[j + 1] = P2[j] + c;
+        Q[j + 1] = Q[j] + ((a + c) - e);
+        const int y = j - 2 * R;
+        if (y >= 0) {
+            const int gy = Y0 + y0 + y;
+            if (BORDER && gy >= H) break;
+            const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                 P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                 P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                 Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+            select_store<R, EXACT_DIV, BORDER, false>(S, Uc[y + R], gx, gy, W, H, b, o, nullptr,
+                                                      nullptr, cf, rtab);
+            o += out_pitch;
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+__global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3 : 2))
+    fast_tma_step(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+                  size_t out_pitch, size_t out_plane, int W, int H) {
+    using Ly = TLay<R, T>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ double rtab[Ly::NRT];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    T* Us = reinterpret_cast<T*>(smem_raw + ((128u - (base & 127u)) & 127u));
+    const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH, b = blockIdx.z;
+    if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
+    if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
+        tma::load_3d(Us, &tmap, X0 - Ly::RA, Y0 - R, b, &bar);
+    }
+    tma::mbar_wait(&bar, 0);
+    double* outp = out + static_cast<size_t>(b) * out_plane;
+    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= H)
+        direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, H, b, outp, out_pitch, rtab);
+    else
+        direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, H, b, outp, out_pitch, rtab);
+}
+
+template <typename T>
+constexpr CUtensorMapDataType tma_dtype() {
+    return sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                          : (sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                            : CU_TENSOR_MAP_DATA_TYPE_UINT8);
+}
+
+// Returns cudaErrorNotSupported (no launch) when the layout is not TMA-able.
+template <int R, typename T, bool EXACT_DIV>
+cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                       size_t opl, cudaStream_t s) {
+    using Ly = TLay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.height) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.height, g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+        return cudaErrorNotSupported;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_tma_step<R, T, EXACT_DIV>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Ly::SMEM));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width, g.height);
+    return cudaGetLastError();
+}
+
 template <int R, bool DIAG>
 cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, size_t op,
                          size_t opl, double* means, uint8_t* sel, cudaStream_t s) {
+    if constexpr (R <= kUnrollRadius && !DIAG) {
+        cudaError_t e = cudaErrorNotSupported;
+        switch (in.dtype) {
+            case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
+            case OSBF_F32: e = launch_tma<R, float, false>(in, g, out, op, opl, s); break;
+            default: e = launch_tma<R, double, false>(in, g, out, op, opl, s); break;
+        }
+        if (e != cudaErrorNotSupported) return e;
+    }
     switch (in.dtype) {
         case OSBF_U8:
             return launch_r<R, uint8_t, true, DIAG>(in, g, out, op, opl, means, sel, s);
