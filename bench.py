@@ -46,7 +46,7 @@ IN_BYTES = {"u8": 1, "f32": 4, "f64": 8}
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
@@ -327,7 +327,8 @@ def run_ours(args, world, rank, local):
     alg_bytes_step = px * ((in_b + 8) + (iters - 1) * 16)
     per_launch_bytes = alg_bytes_step / iters
     if args.mode == "fast":
-        kernel = "fast_tile_step"
+        # R <= 4: TMA-staged direct kernel; larger radii: two-phase kernel
+        kernel = "fast_tma_step" if r <= 4 else "fast_sep_step"
         kernel_ms = sum(step_ms) / (args.steps * iters)
         launches_per_pass = 1
     else:
