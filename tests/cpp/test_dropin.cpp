@@ -1,0 +1,262 @@
+// C++ drop-in test: the reference's hot-path test cases (proj/tests/
+// test_core.cpp, test_integral.cpp, test_filters2d.cpp, acceptance.cpp
+// criteria 1, 2, 5) re-expressed against include/osbf/*.hpp, which run on the
+// GPU through libosbf_gpu.so.  The CPU checker is the oracle restatement
+// (oracle/osbf_oracle.c; test infrastructure only).  Prints one PASS/FAIL
+// line per case; exit code = number of failures.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "osbf/osbf.hpp"
+#include "osbf_oracle.h"
+
+using osbf::ImagePlane;
+
+namespace {
+
+int failures = 0;
+
+void run(const char* name, const std::function<bool()>& fn) {
+    bool ok = false;
+    std::string why;
+    try {
+        ok = fn();
+    } catch (const std::exception& e) {
+        why = e.what();
+    }
+    std::printf("%s %s%s%s\n", ok ? "PASS" : "FAIL", name, why.empty() ? "" : ": ", why.c_str());
+    if (!ok) ++failures;
+}
+
+template <typename E, typename F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// fixtures::random_plane equivalent (mt19937_64, 53-bit uniform on [lo,hi)).
+ImagePlane random_plane(int w, int h, std::uint64_t seed, double lo = 0.0, double hi = 255.0) {
+    ImagePlane p(w, h);
+    std::mt19937_64 rng(seed);
+    for (double& v : p.samples()) v = lo + (hi - lo) * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+    return p;
+}
+
+ImagePlane step(int w, int h, int edge, double lo, double hi) {
+    ImagePlane p(w, h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) p(x, y) = x < edge ? lo : hi;
+    return p;
+}
+
+ImagePlane checkerboard(int w, int h, int cell, double lo, double hi) {
+    ImagePlane p(w, h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) p(x, y) = ((x / cell + y / cell) % 2 == 0) ? lo : hi;
+    return p;
+}
+
+double max_abs_diff(const ImagePlane& a, const ImagePlane& b) {
+    double m = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.samples()[i] - b.samples()[i]));
+    return m;
+}
+
+bool bit_equal(const ImagePlane& a, const ImagePlane& b) {
+    return a.same_size(b) &&
+           std::memcmp(a.samples().data(), b.samples().data(), a.size() * sizeof(double)) == 0;
+}
+
+ImagePlane checker_osbf(const ImagePlane& p, int r, int it) {
+    ImagePlane out(p.width(), p.height());
+    if (oracle_osbf(p.samples().data(), out.samples().data(), p.width(), p.height(), r, it) != 0)
+        throw std::runtime_error("oracle failed");
+    return out;
+}
+
+}  // namespace
+
+int main() {
+    // ---- core.hpp (test_core.cpp:95-114)
+    run("sub-window geometry", [] {
+        const int r = 3;
+        const auto w = osbf::sub_windows(r);
+        for (int i = 0; i < 8; ++i) {
+            const auto& s = w[static_cast<size_t>(i)];
+            if (s.id != i + 1 || s.u0 > 0 || s.u1 < 0 || s.v0 > 0 || s.v1 < 0) return false;
+            const long long px = static_cast<long long>(s.u1 - s.u0 + 1) * (s.v1 - s.v0 + 1);
+            if (px != (i < 4 ? (r + 1) * (r + 1) : (r + 1) * (2 * r + 1))) return false;
+        }
+        return throws<std::invalid_argument>([] { osbf::sub_windows(0); });
+    });
+    run("ImagePlane errors", [] {
+        return throws<std::invalid_argument>([] { ImagePlane(0, 3); }) &&
+               throws<std::out_of_range>([] { ImagePlane(2, 2).get(2, 0); });
+    });
+
+    // ---- integral.hpp (test_integral.cpp:19-29, 42-47, 80-89)
+    run("summed-area table prefix sums", [] {
+        const auto sat = osbf::build_sat(ImagePlane(2, 2, std::vector<double>{1, 2, 3, 4}));
+        return sat.cumsum(0, 0) == 0.0 && sat.cumsum(2, 0) == 0.0 && sat.cumsum(0, 2) == 0.0 &&
+               sat.cumsum(1, 1) == 1.0 && sat.cumsum(2, 1) == 3.0 && sat.cumsum(1, 2) == 4.0 &&
+               sat.cumsum(2, 2) == 10.0;
+    });
+    run("SAT bit-identical to the reference order", [] {
+        const auto p = random_plane(37, 23, 11);
+        const auto sat = osbf::build_sat(p);
+        std::vector<double> want(38 * 24);
+        oracle_sat_build(p.samples().data(), 37, 23, want.data());
+        for (int y = 0; y <= 23; ++y)
+            for (int x = 0; x <= 37; ++x)
+                if (sat.cumsum(x, y) != want[static_cast<size_t>(y) * 38 + x]) return false;
+        return true;
+    });
+    run("rect_sum / rect_mean basics", [] {
+        const auto ones = osbf::build_sat(ImagePlane(5, 5, 1.0));
+        const auto c = osbf::build_sat(ImagePlane(6, 4, 3.25));
+        const auto tiny = osbf::build_sat(ImagePlane(2, 1, std::vector<double>{0, 100}));
+        return osbf::rect_sum(ones, 1, 1, 3, 3) == 9.0 && osbf::rect_sum(ones, 10, 10, 20, 20) == 0.0 &&
+               osbf::rect_mean(c, 0, 0, 5, 3) == 3.25 && osbf::rect_mean(c, -3, -3, 2, 2) == 3.25 &&
+               osbf::rect_mean(tiny, 0, 0, 1, 0) == 50.0 &&
+               throws<std::domain_error>([&] { osbf::rect_mean(c, 10, 10, 12, 12); });
+    });
+
+    // ---- filters2d.hpp (test_filters2d.cpp)
+    run("subwindow means on a constant plane", [] {
+        const auto sat = osbf::build_sat(ImagePlane(10, 10, 7.25));
+        for (double a : osbf::subwindow_means(sat, 4, 5, 2).a)
+            if (a != 7.25) return false;
+        return true;
+    });
+    run("left half window stays on the low side of a step", [] {
+        const auto sat = osbf::build_sat(step(16, 16, 8, 0.0, 100.0));
+        for (int r : {1, 2, 3})
+            if (osbf::subwindow_means(sat, 7, 8, r).a[4] != 0.0) return false;
+        return true;
+    });
+    for (osbf::gpu::Mode mode : {osbf::gpu::Mode::Exact, osbf::gpu::Mode::Fast}) {
+        const std::string tag = mode == osbf::gpu::Mode::Exact ? " [exact]" : " [fast]";
+        osbf::gpu::ScopedMode scoped(mode);
+        run(("osbf_step keeps constant planes" + tag).c_str(), [] {
+            const ImagePlane p(9, 9, 3.5);
+            return max_abs_diff(osbf::osbf_step(p, 2), p) == 0.0;
+        });
+        run(("osbf_step keeps ideal vertical steps" + tag).c_str(), [] {
+            for (int r : {1, 2, 5, 8}) {
+                const auto p = step(32, 16, 16, 0.0, 100.0);
+                if (max_abs_diff(osbf::osbf_step(p, r), p) != 0.0) return false;
+            }
+            return true;
+        });
+        run(("checkerboards with cell >= 2r are fixed points" + tag).c_str(), [] {
+            for (int r : {1, 2, 3}) {
+                const auto p = checkerboard(8 * r, 8 * r, 2 * r, 0.0, 255.0);
+                const auto q = checkerboard(64, 64, 2 * r + 3, 10.0, 200.0);
+                if (max_abs_diff(osbf::osbf_step(p, r), p) != 0.0) return false;
+                if (max_abs_diff(osbf::osbf_step(q, r), q) != 0.0) return false;
+            }
+            return max_abs_diff(osbf::osbf_step(checkerboard(32, 32, 4, 0.0, 255.0), 3),
+                                checkerboard(32, 32, 4, 0.0, 255.0)) > 1.0;
+        });
+        run(("step stays fixed for 30 iterations" + tag).c_str(), [] {
+            const auto p = step(64, 32, 32, 0.0, 100.0);
+            return max_abs_diff(osbf::osbf(p, 2, 30), p) == 0.0;
+        });
+        run(("zero iterations is the identity; argument errors" + tag).c_str(), [] {
+            const auto p = random_plane(10, 10, 3);
+            return bit_equal(osbf::osbf(p, 2, 0), p) && bit_equal(osbf::osbf(p, 0, 0), p) &&
+                   throws<std::invalid_argument>([&] { osbf::osbf(p, 2, -1); }) &&
+                   throws<std::invalid_argument>([&] { osbf::osbf(p, 0, 1); }) &&
+                   throws<std::invalid_argument>([&] { osbf::osbf_step(p, 0); });
+        });
+        run(("range preservation" + tag).c_str(), [] {
+            const auto p = random_plane(20, 20, 17, 10.0, 90.0);
+            double lo = 1e300, hi = -1e300;
+            for (double v : p.samples()) lo = std::min(lo, v), hi = std::max(hi, v);
+            const auto out = osbf::osbf(p, 2, 5);
+            for (double v : out.samples())
+                if (v < lo || v > hi) return false;
+            return true;
+        });
+        run(("filter_multichannel applies per channel" + tag).c_str(), [] {
+            osbf::FilterConfig cfg;
+            cfg.radius = 2;
+            cfg.iterations = 2;
+            const osbf::MultiChannelImage rgb(
+                {random_plane(12, 12, 1), random_plane(12, 12, 2), random_plane(12, 12, 3)});
+            const auto out = osbf::filter_multichannel(rgb, cfg);
+            for (int c = 0; c < 3; ++c)
+                if (!bit_equal(out.channel(c), osbf::osbf(rgb.channel(c), 2, 2))) return false;
+            osbf::FilterConfig bad = cfg;
+            bad.radius = 0;
+            osbf::FilterConfig box = cfg;
+            box.variant = osbf::FilterVariant::Box;
+            return throws<std::invalid_argument>([&] { osbf::filter_multichannel(rgb, bad); }) &&
+                   throws<std::invalid_argument>([&] { osbf::filter_multichannel(rgb, box); });
+        });
+        run(("outputs identical for any thread cap" + tag).c_str(), [] {
+            const auto p = random_plane(33, 29, 123);
+            osbf::set_max_threads(1);
+            const auto a = osbf::osbf(p, 2, 2);
+            osbf::set_max_threads(4);
+            const auto b = osbf::osbf(p, 2, 2);
+            osbf::set_max_threads(0);
+            return bit_equal(a, b);
+        });
+    }
+    run("osbf bit-identical to the oracle (24x24, r in {1,2,3,5}, 3 it) [exact]", [] {
+        for (int r : {1, 2, 3, 5}) {
+            const auto p = random_plane(24, 24, 200 + r);
+            if (!bit_equal(osbf::osbf(p, r, 3), checker_osbf(p, r, 3))) return false;
+        }
+        return true;
+    });
+    run("osbf within 1e-9 of the oracle [fast]", [] {
+        osbf::gpu::ScopedMode fast(osbf::gpu::Mode::Fast);
+        for (int r : {1, 2, 3, 5}) {
+            const auto p = random_plane(24, 24, 200 + r);
+            if (max_abs_diff(osbf::osbf(p, r, 3), checker_osbf(p, r, 3)) > 1e-9) return false;
+        }
+        return true;
+    });
+
+    // ---- acceptance.cpp criteria 1, 2, 5
+    run("acceptance 1: edge fixed point (256^2, r in {1,2,5,10}, 30 it)", [] {
+        double worst = 0.0;
+        for (int r : {1, 2, 5, 10}) {
+            const auto p = step(256, 256, 128, 100.0, 200.0);
+            worst = std::max(worst, max_abs_diff(osbf::osbf(p, r, 30), p));
+        }
+        return worst <= 1e-6;
+    });
+    run("acceptance 2: corner fixed point (cell 32, r 1..10)", [] {
+        const auto board = checkerboard(256, 256, 32, 0.0, 255.0);
+        double worst = 0.0;
+        for (int r = 1; r <= 10; ++r) worst = std::max(worst, max_abs_diff(osbf::osbf(board, r, 1), board));
+        return worst <= 1e-6;
+    });
+    run("acceptance 5: 50 planes 64x64, r in {1,2,3,5}, 3 it, bit-identical to the oracle", [] {
+        for (int k = 0; k < 50; ++k) {
+            const auto p = random_plane(64, 64, 1000 + k);
+            for (int r : {1, 2, 3, 5})
+                if (!bit_equal(osbf::osbf(p, r, 3), checker_osbf(p, r, 3))) return false;
+        }
+        return true;
+    });
+
+    std::printf("%d failure(s)\n", failures);
+    return failures;
+}

@@ -93,3 +93,13 @@ def test_python_value_types_mirror_reference():
     cfg = ob.FilterConfig(iterations=-1)
     with pytest.raises(ValueError):
         cfg.validate()
+
+
+def test_dropin_headers_compile_and_link():
+    """include/osbf/*.hpp (the reference's declarations) compile and the C++
+    drop-in test links against libosbf_gpu.so (run on the GPU by test_dropin_gpu)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    assert os.path.exists(exe)
+    out = subprocess.run(["nm", "-D", exe], capture_output=True, text=True, check=True).stdout
+    assert "osbf_gpu_osbf_host" in out and "oracle_osbf" in out
