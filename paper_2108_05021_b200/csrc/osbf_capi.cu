@@ -126,7 +126,14 @@ cudaStream_t pick_stream(osbf_ctx*, void* stream) { return static_cast<cudaStrea
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
                      int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
                      osbf_mode mode, cudaStream_t s) {
-    if (mode == OSBF_MODE_EXACT) {
+    if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius) {
+        // fused exact path: row carries + strip kernel (same bits as below)
+        OSBF_CUDA(ctx->rowpfx.ensure(osbf_gpu::exact_fused_carry_elems(g) * sizeof(double)),
+                  "alloc carries");
+        OSBF_CUDA(osbf_gpu::exact_fused_step(src, g, r, ctx->rowpfx.as<double>(), dst, dp, dpl, s,
+                                             ctx->lc),
+                  "exact fused step");
+    } else if (mode == OSBF_MODE_EXACT) {
         const size_t n = static_cast<size_t>(g.batch) * g.width * g.height;
         const size_t ns = static_cast<size_t>(g.batch) * (g.width + 1) * (g.height + 1);
         OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");

@@ -14,6 +14,7 @@
 //                         count (integral.hpp:68), |a-u|, strict < in window
 //                         order, write a_m itself (filters2d.hpp:80-83).
 // All fp64 arithmetic uses the _rn intrinsics so nothing is contracted.
+#include "osbf_exact2_kernel.cuh"
 #include "osbf_internal.cuh"
 
 namespace osbf_gpu {
@@ -187,6 +188,62 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
             return launch_stencil<double>(in, g, radius, sat, out, out_pitch, out_plane, means,
                                           sel, s);
     }
+}
+
+// ---- fused exact path (osbf_exact2_kernel.cuh) ------------------------------
+
+namespace {
+using Exact2Fn = cudaError_t (*)(const PlaneView&, const Geometry&, double*, int, double*, size_t,
+                                 size_t, cudaStream_t);
+constexpr Exact2Fn kExact2[kExactFusedMaxRadius + 1] = {
+    nullptr,
+    exact2_launch_radius<1>,  exact2_launch_radius<2>,  exact2_launch_radius<3>,
+    exact2_launch_radius<4>,  exact2_launch_radius<5>,  exact2_launch_radius<6>,
+    exact2_launch_radius<7>,  exact2_launch_radius<8>,  exact2_launch_radius<9>,
+    exact2_launch_radius<10>, exact2_launch_radius<11>, exact2_launch_radius<12>,
+    exact2_launch_radius<13>, exact2_launch_radius<14>, exact2_launch_radius<15>,
+    exact2_launch_radius<16>,
+};
+static_assert(kExactFusedMaxRadius == 16, "update kExact2");
+
+template <typename T>
+cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carries, int nsc,
+                           cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(ex2::exact_row_carries<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(ex2::K1_SMEM));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const long long rows = static_cast<long long>(g.batch) * g.height;
+    const long long ctas = (rows + ex2::NTK1 - 1) / ex2::NTK1;
+    ex2::exact_row_carries<T><<<static_cast<unsigned>(ctas), ex2::NTK1, ex2::K1_SMEM, s>>>(
+        static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height, rows, nsc);
+    return cudaGetLastError();
+}
+}  // namespace
+
+size_t exact_fused_carry_elems(const Geometry& g) {
+    return static_cast<size_t>(g.batch) * g.height * (g.width / ex2::SW + 1);
+}
+
+cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius, double* carries,
+                             double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
+                             LaunchCounter& lc) {
+    if (radius < 1 || radius > kExactFusedMaxRadius) return cudaErrorInvalidValue;
+    const int nsc = g.width / ex2::SW + 1;
+    cudaError_t e;
+    switch (in.dtype) {
+        case OSBF_U8: e = launch_carries<uint8_t>(in, g, carries, nsc, s); break;
+        case OSBF_F32: e = launch_carries<float>(in, g, carries, nsc, s); break;
+        default: e = launch_carries<double>(in, g, carries, nsc, s); break;
+    }
+    ++lc.launches;
+    if (e != cudaSuccess) return e;
+    ++lc.launches;
+    return kExact2[radius](in, g, carries, nsc, out, out_pitch, out_plane, s);
 }
 
 }  // namespace osbf_gpu

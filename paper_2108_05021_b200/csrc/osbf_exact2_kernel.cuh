@@ -1,0 +1,423 @@
+// Exact mode, fused path: bit-identical to the reference, O(1) HBM passes.
+//
+// The reference's table (integral.hpp:16-30) is the serial fp64 recurrence
+//     R(x,y) = R(x-1,y) + U(x,y)          (row running sum, left to right)
+//     C(x+1,y+1) = C(x+1,y) + R(x,y)      (table column, top to bottom)
+// and every window sum is ((A-B)-C)+D over it (integral.hpp:48-49).  Any
+// re-association changes roundings that decide exact ties, so this path
+// replays the recurrence in the same order, split across two kernels:
+//
+//  K1 exact_row_carries : one serial chain per row (H*B chains); stores only
+//                         the carries R(16s-1, y) (every SW=16 columns).
+//  K2 exact_strip       : one CTA per TW=32-column strip of one plane walks
+//                         the plane top to bottom in blocks of BR=32 rows:
+//      L  stage U rows of the block (columns from the carry boundary left of
+//         the halo to the right halo), cp.async for fp64 input
+//      RR thread-per-row: continue R from the stored carry across the strip
+//         (same serial adds as the reference)
+//      CC thread-per-table-column: continue C down the block, into a ring
+//      S  stencil of the PREVIOUS block's rows (their windows need table rows
+//         up to y+R+1): 8 clipped ((A-B)-C)+D sums, division by the valid
+//         count, |a-u|, strict < in window order, write a_m
+//         (filters2d.hpp:69-84).
+//
+// Division: s/n for a positive integer n is computed as
+//     q0 = s*y, r = fma(-q0, n, s) (exact), q = fma(r, y, q0), y = RN(1/n)
+// which is the IEEE quotient: the exact s/n is never a rounding midpoint for
+// an integer divisor, and q0 + r*y is within 1.5*2^-53 ulp of it, far closer
+// than any midpoint (>= ulp/(4n) away).  tools/probes/divcheck.c and
+// tests/test_division.py check it (exhaustively over the uint8 domain).
+// Non-normal magnitudes take __ddiv_rn.
+#pragma once
+
+#include "osbf_internal.cuh"
+
+namespace osbf_gpu {
+
+// Out of line so the compiler cannot if-convert (speculate) it into the fast path.
+static __device__ __noinline__ double div_slow(double s, double n) { return __ddiv_rn(s, n); }
+
+// IEEE-exact s / n for a positive integer n with precomputed y = RN(1/n),
+// valid when s == 0 or |s| in [2^-900, 2^900] (normal, finite quotient).
+__device__ __forceinline__ double div_by_count_unguarded(double s, double n, double y) {
+    const double q0 = __dmul_rn(s, y);
+    const double r = __fma_rn(-q0, n, s);
+    return __fma_rn(r, y, q0);
+}
+
+// Same, for any s (subnormal quotients and non-finite sums take __ddiv_rn).
+__device__ __forceinline__ double div_by_count(double s, double n, double y) {
+    const double q = div_by_count_unguarded(s, n, y);
+    const unsigned hi = static_cast<unsigned>(__double2hiint(s)) & 0x7ff00000u;
+    if (s != 0.0 && (hi - (123u << 20)) > ((1923u - 123u) << 20)) return div_slow(s, n);
+    return q;
+}
+
+// A table value is "safe" when it is 0 or |v| in [2^-800, 2^900]: then every
+// window sum ((A-B)-C)+D of safe values is 0 or a multiple of 2^-852 below
+// 2^902, so div_by_count_unguarded is exact for it.
+__device__ __forceinline__ bool table_value_safe(double v) {
+    const unsigned e = static_cast<unsigned>(__double2hiint(v)) & 0x7ff00000u;
+    return v == 0.0 || (e - (223u << 20)) <= ((1923u - 223u) << 20);
+}
+
+namespace ex2 {
+
+constexpr int TW = 32;   // output columns per strip
+constexpr int SW = 16;   // spacing of the stored row carries (columns)
+constexpr int BR = 32;   // rows per block
+constexpr int NT = 256;  // threads per strip CTA
+constexpr int NTK1 = 64; // threads per carry CTA (2 warps, 32 rows each)
+
+template <int R>
+struct XLay {
+    // staged U columns: [xs, xs + NU) with xs = floor((X0-R)/SW)*SW >= X0-R-SW+1,
+    // covering up to X0 + TW + R - 1
+    static constexpr int NU = TW + 2 * R + SW;
+    // pitch = 2 (mod 4) doubles: 16-byte aligned rows for 16-byte cp.async,
+    // at most 2-way conflicts on the lanes = rows walk
+    static constexpr int PUB = (NU % 4 == 2) ? NU : NU + 2;
+    static constexpr int NCC = TW + 2 * R + 1;  // table columns cx in [X0-R, X0+TW+R]
+    static constexpr int PR = NCC | 1;
+    // table rows kept: [y0-BR-R, y0+BR] (2BR+R+1 rows), as a power of two
+    static constexpr int NRING = (2 * BR + R + 2) <= 128 ? 128 : 256;
+    static constexpr int U_ELEMS = BR * PUB;
+    static constexpr size_t SMEM =
+        sizeof(double) * (3 * static_cast<size_t>(U_ELEMS) + BR * PR + NRING * NCC + 2 * BR);
+};
+
+}  // namespace ex2
+}  // namespace osbf_gpu
+
+namespace osbf_gpu {
+namespace ex2 {
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K1: row carries.  carries[g*nsc + s] = R(s*SW - 1, y) for s >= 1, 0 for s = 0
+// (g = b*H + y).  One warp walks 32 rows; 32-column chunks are transposed
+// through shared memory (lane = column on the load, lane = row on the scan)
+// with a 3-stage cp.async ring for fp64 input.
+constexpr int K1_STAGES = 3;
+constexpr size_t K1_SMEM = sizeof(double) * (NTK1 / 32) * K1_STAGES * 32 * 33;
+
+template <typename T>
+__global__ void __launch_bounds__(NTK1)
+    exact_row_carries(const T* __restrict__ in, size_t pitch, size_t plane,
+                      double* __restrict__ carries, int W, int H, long long rows, int nsc) {
+    extern __shared__ double k1s[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long row0 = (static_cast<long long>(blockIdx.x) * (NTK1 / 32) + warp) * 32;
+    if (row0 >= rows) return;
+    double* ring = k1s + static_cast<size_t>(warp) * K1_STAGES * 32 * 33;
+    long long my_base = -1;
+    {
+        const long long g = row0 + lane;
+        if (g < rows) {
+            const long long b = g / H, y = g - b * H;
+            my_base = b * static_cast<long long>(plane) + y * static_cast<long long>(pitch);
+        }
+    }
+    const int nchunks = (W + 31) / 32;
+    auto issue = [&](int c) {
+        double* t = ring + (c % K1_STAGES) * 32 * 33;
+        const int x = 32 * c + lane;
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const long long base = __shfl_sync(0xffffffffu, my_base, rr);
+            const bool ok = base >= 0 && x < W;
+            if constexpr (sizeof(T) == 8) {
+                cp_async8(t + lane * 33 + rr, reinterpret_cast<const double*>(in) + (ok ? base + x : 0),
+                          ok);
+            } else {
+                t[lane * 33 + rr] = ok ? to_f64(in[base + x]) : 0.0;
+            }
+        }
+        cp_commit();
+    };
+    for (int c = 0; c < K1_STAGES - 1; ++c) {
+        if (c < nchunks) issue(c);
+        else cp_commit();
+    }
+    double acc = 0.0;
+    const long long g = row0 + lane;
+    double* crow = carries + (g < rows ? g : 0) * nsc;
+    if (g < rows) crow[0] = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + K1_STAGES - 1 < nchunks) issue(c + K1_STAGES - 1);
+        else cp_commit();
+        cp_wait<K1_STAGES - 1>();
+        __syncwarp();
+        const double* t = ring + (c % K1_STAGES) * 32 * 33;
+        const int n = min(32, W - 32 * c);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            if (k < n) {
+                acc = __dadd_rn(acc, t[k * 33 + lane]);  // row += src[x]  (integral.hpp:25)
+                if ((k + 1) % SW == 0 && g < rows) crow[(32 * c + k + 1) / SW] = acc;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused strip kernel (see the header comment).
+template <int R, typename T>
+__device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pitch,
+                                            const double* __restrict__ carries, int nsc, int s0,
+                                            long long gbase, int xs, int y0, int W, int H,
+                                            double* __restrict__ U, double* __restrict__ cs,
+                                            bool aligned16) {
+    using L = XLay<R>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (sizeof(T) == 8) {
+        // warp per row, 16-byte copies (xs is a multiple of SW = 16 columns)
+        const bool vec = aligned16;
+        for (int rr = warp; rr < BR; rr += NT / 32) {
+            const int y = y0 + rr;
+            const double* row = reinterpret_cast<const double*>(src) +
+                                static_cast<size_t>(y < H ? y : 0) * pitch;
+            double* d = U + rr * L::PUB;
+            if (vec) {
+                for (int p = lane; p < L::NU / 2; p += 32) {
+                    const int x = xs + 2 * p;
+                    const int nbytes = (y < H && x < W) ? (x + 1 < W ? 16 : 8) : 0;
+                    const unsigned da = static_cast<unsigned>(__cvta_generic_to_shared(d + 2 * p));
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(da),
+                                 "l"(row + (nbytes ? x : 0)), "r"(nbytes));
+                }
+            } else {
+                for (int i = lane; i < L::NU; i += 32) {
+                    const int x = xs + i;
+                    const bool ok = y < H && x < W;
+                    cp_async8(d + i, row + (ok ? x : 0), ok);
+                }
+            }
+        }
+    } else {
+        for (int rr = warp; rr < BR; rr += NT / 32) {
+            const int y = y0 + rr;
+            for (int i = lane; i < L::NU; i += 32) {
+                const int x = xs + i;
+                U[rr * L::PUB + i] =
+                    (y < H && x < W) ? to_f64(src[static_cast<size_t>(y) * pitch + x]) : 0.0;
+            }
+        }
+    }
+    if (threadIdx.x < BR) {
+        const int y = y0 + threadIdx.x;
+        cs[threadIdx.x] = y < H ? carries[(gbase + y) * nsc + s0] : 0.0;
+    }
+    cp_commit();
+}
+
+template <int R>
+__device__ __forceinline__ int ring_row(int cy) {
+    return cy & (XLay<R>::NRING - 1);
+}
+
+// Stencil of rows [yb, yb + nrows) for output column x (lane-owned).  SAFE:
+// every table value of the strip so far passed table_value_safe.
+template <int R, bool SAFE>
+__device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
+                                             const double* __restrict__ U, int xs, int X0, int yb,
+                                             int nrows, int W, int H, double* __restrict__ outp,
+                                             size_t opitch) {
+    using L = XLay<R>;
+    const int lx = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int x = X0 + lx;
+    if (x >= W) return;
+    const int cbase = X0 - R;  // table column of Cr index 0
+    constexpr double kYq = 1.0 / ((R + 1) * (R + 1));
+    constexpr double kYh = 1.0 / ((R + 1) * (2 * R + 1));
+    constexpr double kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
+    const bool col_int = x >= R && x + R < W;
+    double* op = outp + static_cast<size_t>(yb + grp) * opitch + x;
+    const size_t ostep = static_cast<size_t>(NT / 32) * opitch;
+    for (int rr = grp; rr < nrows; rr += NT / 32, op += ostep) {
+        const int y = yb + rr;
+        const double u = U[rr * L::PUB + (x - xs)];
+        double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
+        if (col_int && y >= R && y + R < H) {
+            // 4x4 corner grid: rows {y-R, y, y+1, y+R+1}, cols {x-R, x, x+1, x+R+1}
+            const double* rp[4] = {Cr + ring_row<R>(y - R) * L::NCC + lx,
+                                   Cr + ring_row<R>(y) * L::NCC + lx,
+                                   Cr + ring_row<R>(y + 1) * L::NCC + lx,
+                                   Cr + ring_row<R>(y + R + 1) * L::NCC + lx};
+            constexpr int co[4] = {0, R, R + 1, 2 * R + 1};
+            double g[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) g[a][c] = rp[a][co[c]];
+            // (ca, cb, ra, rb) per window in reference order (core.hpp:212-225)
+            constexpr int W8[8][4] = {{0, 2, 1, 3}, {1, 3, 1, 3}, {1, 3, 0, 2}, {0, 2, 0, 2},
+                                      {0, 2, 0, 3}, {1, 3, 0, 3}, {0, 3, 1, 3}, {0, 3, 0, 2}};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int ca = W8[i][0], cb = W8[i][1], ra = W8[i][2], rb = W8[i][3];
+                const double s =
+                    __dadd_rn(__dsub_rn(__dsub_rn(g[rb][cb], g[rb][ca]), g[ra][cb]), g[ra][ca]);
+                const double a = SAFE ? div_by_count_unguarded(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh)
+                                      : div_by_count(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh);
+                const double d = fabs(__dsub_rn(a, u));
+                if (d < best_abs) {
+                    best_abs = d;
+                    best = a;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const Win w = window(i, R);
+                const int x0 = max(x + w.u0, 0), x1 = min(x + w.u1, W - 1);
+                const int y0 = max(y + w.v0, 0), y1 = min(y + w.v1, H - 1);
+                const double* ra = Cr + ring_row<R>(y0) * L::NCC;
+                const double* rb = Cr + ring_row<R>(y1 + 1) * L::NCC;
+                const double A = rb[x1 + 1 - cbase], Bv = rb[x0 - cbase];
+                const double Cv = ra[x1 + 1 - cbase], D = ra[x0 - cbase];
+                const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
+                const double n = static_cast<double>((x1 - x0 + 1) * (y1 - y0 + 1));
+                const double a = div_by_count(s, n, __ddiv_rn(1.0, n));
+                const double d = fabs(__dsub_rn(a, u));
+                if (d < best_abs) {
+                    best_abs = d;
+                    best = a;
+                }
+            }
+        }
+        *op = best;
+    }
+}
+
+template <int R, typename T>
+__global__ void __launch_bounds__(NT, 1)
+    exact_strip(const T* __restrict__ in, size_t pitch, size_t plane,
+                const double* __restrict__ carries, int nsc, double* __restrict__ out,
+                size_t opitch, size_t oplane, int W, int H) {
+    using L = XLay<R>;
+    extern __shared__ double sm[];
+    double* Ubuf = sm;                          // 3 x [BR][PUB]
+    double* Rb = sm + 3 * L::U_ELEMS;           // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
+    double* Cr = Rb + BR * L::PR;               // [NRING][NCC]: table rows, column cx = X0-R+t
+    double* cs = Cr + L::NRING * L::NCC;        // 2 x [BR] staged carries
+    const int b = blockIdx.y;
+    const int X0 = blockIdx.x * TW;
+    const int xs_raw = X0 - R;
+    const int xs = xs_raw <= 0 ? 0 : (xs_raw / SW) * SW;
+    const int s0 = xs / SW;
+    const T* src = in + static_cast<size_t>(b) * plane;
+    double* outp = out + static_cast<size_t>(b) * oplane;
+    const long long gbase = static_cast<long long>(b) * H;
+    const int nblocks = (H + BR - 1) / BR;
+    const int tid = threadIdx.x;
+    const int xe = min(X0 + TW + R - 1, W - 1);  // last R column needed
+
+    double creg = 0.0;    // running table column (threads < NCC)
+    bool unsafe = false;  // some table value outside the unguarded-division range
+    if (tid < L::NCC) Cr[ring_row<R>(0) * L::NCC + tid] = 0.0;  // zero border row
+    const bool aligned16 = sizeof(T) == 8 && (pitch % 2 == 0) &&
+                           (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, 0, W, H, Ubuf, cs, aligned16);
+    for (int k = 0; k < nblocks; ++k) {
+        const int y0 = k * BR;
+        const int nrows = min(BR, H - y0);
+        if (k + 1 < nblocks)
+            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + BR, W, H,
+                              Ubuf + ((k + 1) % 3) * L::U_ELEMS, cs + ((k + 1) & 1) * BR,
+                              aligned16);
+        else
+            cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        // RR: continue the row running sums from the stored carries.
+        if (tid < BR) {
+            const double* u = Ubuf + (k % 3) * L::U_ELEMS + tid * L::PUB;
+            double* rb = Rb + tid * L::PR;
+            const int jfirst = xs - 1 - (X0 - R - 1);
+            for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;  // x < -1 (strip 0)
+            double acc = cs[(k & 1) * BR + tid];  // R(xs - 1)
+            if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = acc;
+            for (int x = xs; x <= xe; ++x) {
+                acc = __dadd_rn(acc, u[x - xs]);
+                const int j = x - (X0 - R - 1);
+                if (j >= 0) rb[j] = acc;
+            }
+        }
+        __syncthreads();
+        // CC: continue the table columns down the block.
+        bool unsafe_here = false;
+        if (tid < L::NCC) {
+            const int cx = X0 - R + tid;
+            if (cx >= 0 && cx <= W) {
+                for (int rr = 0; rr < nrows; ++rr) {
+                    creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);  // above[x+1] + row
+                    unsafe_here |= !table_value_safe(creg);
+                    Cr[ring_row<R>(y0 + rr + 1) * L::NCC + tid] = creg;
+                }
+            }
+        }
+        unsafe = __syncthreads_or(unsafe || unsafe_here);  // sticky for the strip
+        // S: previous block's rows now have every table row they need.
+        if (k > 0) {
+            if (!unsafe)
+                stencil_rows<R, true>(Cr, Ubuf + ((k - 1) % 3) * L::U_ELEMS, xs, X0, y0 - BR, BR,
+                                      W, H, outp, opitch);
+            else
+                stencil_rows<R, false>(Cr, Ubuf + ((k - 1) % 3) * L::U_ELEMS, xs, X0, y0 - BR, BR,
+                                       W, H, outp, opitch);
+        }
+        __syncthreads();
+    }
+    const int ylast = (nblocks - 1) * BR;
+    if (!unsafe)
+        stencil_rows<R, true>(Cr, Ubuf + ((nblocks - 1) % 3) * L::U_ELEMS, xs, X0, ylast,
+                              H - ylast, W, H, outp, opitch);
+    else
+        stencil_rows<R, false>(Cr, Ubuf + ((nblocks - 1) % 3) * L::U_ELEMS, xs, X0, ylast,
+                               H - ylast, W, H, outp, opitch);
+}
+
+}  // namespace ex2
+
+// One radius (instantiated in osbf_exact2_rNN.cu).
+template <int R>
+cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double* carries,
+                                 int nsc, double* out, size_t opitch, size_t oplane,
+                                 cudaStream_t s) {
+    using L = ex2::XLay<R>;
+    dim3 grid((g.width + ex2::TW - 1) / ex2::TW, g.batch);
+    auto go = [&](auto tag) -> cudaError_t {
+        using T = decltype(tag);
+        static bool configured = false;
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(ex2::exact_strip<R, T>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(L::SMEM));
+            if (e != cudaSuccess) return e;
+            configured = true;
+        }
+        ex2::exact_strip<R, T><<<grid, ex2::NT, L::SMEM, s>>>(
+            static_cast<const T*>(in.base), in.pitch, in.plane, carries, nsc, out, opitch, oplane,
+            g.width, g.height);
+        return cudaGetLastError();
+    };
+    switch (in.dtype) {
+        case OSBF_U8: return go(uint8_t{});
+        case OSBF_F32: return go(float{});
+        default: return go(double{});
+    }
+}
+
+}  // namespace osbf_gpu

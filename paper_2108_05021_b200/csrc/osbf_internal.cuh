@@ -43,6 +43,14 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
                          double* out, size_t out_pitch, size_t out_plane, double* means,
                          uint8_t* sel, cudaStream_t s, LaunchCounter& lc);
 
+// Fused exact path (osbf_exact2_kernel.cuh): row carries + strip kernel.
+// Bit-identical to exact_build_sat + exact_select; radius <= kExactFusedMaxRadius.
+constexpr int kExactFusedMaxRadius = 16;
+size_t exact_fused_carry_elems(const Geometry& g);
+cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius, double* carries,
+                             double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
+                             LaunchCounter& lc);
+
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
 // Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
 constexpr int kFastMaxRadius = 16;

@@ -55,7 +55,7 @@ def test_launch_counter_counts_kernels(ctx):
     x = torch.rand((64, 64), dtype=torch.float64, device="cuda")
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="exact")
-    assert ctx.launches - before == 9  # 3 kernels per exact pass
+    assert ctx.launches - before == 6  # 2 kernels per exact pass (row carries + strip)
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="fast")
     assert ctx.launches - before == 3
