@@ -123,6 +123,21 @@ osbf_status osbf_gpu_sat(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in, s
                          size_t in_plane_stride, int width, int height, int batch,
                          double* d_cumsum, void* stream);
 
+/*
+ * One FAST-mode pass over a row band of a taller image (multi-GPU row-band
+ * partitioning).  d_in holds global rows [in_row0, in_row0 + in_rows) — the
+ * band plus `radius` halo rows on each side where the image has them;
+ * d_out receives global rows [out_row0, out_row0 + out_rows).  Windows clip
+ * at the global image [0, image_height), so the union of the bands equals a
+ * pass over the whole image (bit-identical when every out_row0 is a multiple
+ * of the 64-row tile).  Exact mode is rejected with INVALID_ARGUMENT: its
+ * whole-image serial prefix (integral.hpp:20-29) cannot be split into bands.
+ */
+osbf_status osbf_gpu_step_band(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                               size_t in_pitch, int in_row0, int in_rows, double* d_out,
+                               size_t out_pitch, int out_row0, int out_rows, int width,
+                               int image_height, int radius, osbf_mode mode, void* stream);
+
 /* ---- host-buffer entry points (what the drop-in C++ API calls) ------------ */
 
 /* osbf::osbf on host memory: copies in, filters, copies out, synchronizes.

@@ -226,6 +226,26 @@ class Context:
             w, h, batch, ctypes.c_void_p(c.data_ptr()), ctypes.c_void_p(stream)))
         return c.view(*src.shape[:-2], h + 1, w + 1)
 
+    def step_band(self, src, in_row0: int, out, out_row0: int, out_rows: int,
+                  image_height: int, radius: int, mode="fast", stream=None):
+        """One fast pass over a row band (osbf_gpu_step_band).  ``src``: CUDA
+        tensor (in_rows, W) holding global rows [in_row0, in_row0+in_rows);
+        ``out``: fp64 CUDA tensor whose rows receive global rows
+        [out_row0, out_row0 + out_rows)."""
+        import torch
+
+        if src.dim() != 2 or out.dim() != 2 or src.stride(1) != 1 or out.stride(1) != 1:
+            raise InvalidArgument("step_band expects 2-D row-major tensors")
+        if out.dtype != torch.float64:
+            raise InvalidArgument("band output must be float64")
+        if stream is None:
+            stream = torch.cuda.current_stream(src.device).cuda_stream
+        _check(self._lib.osbf_gpu_step_band(
+            self.handle, _dtype_code(src), ctypes.c_void_p(src.data_ptr()), src.stride(0), in_row0,
+            src.shape[0], ctypes.c_void_p(out.data_ptr()), out.stride(0), out_row0, out_rows,
+            src.shape[1], image_height, radius, _mode_code(mode), ctypes.c_void_p(stream)))
+        return out
+
     # -- host arrays (the drop-in path: H2D, filter, D2H inside the call) ----
     def osbf_host(self, planes: np.ndarray, radius: int, iterations: int, mode="exact",
                   out: np.ndarray | None = None) -> np.ndarray:

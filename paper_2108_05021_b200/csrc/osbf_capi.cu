@@ -348,6 +348,49 @@ osbf_status osbf_gpu_sat(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in, s
     return OSBF_OK;
 }
 
+osbf_status osbf_gpu_step_band(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                               size_t in_pitch, int in_row0, int in_rows, double* d_out,
+                               size_t out_pitch, int out_row0, int out_rows, int width,
+                               int image_height, int radius, osbf_mode mode, void* stream) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if ((st = check_mode(mode)) != OSBF_OK) return st;
+    if (mode != OSBF_MODE_FAST)
+        return fail(OSBF_ERR_INVALID_ARGUMENT,
+                    "row bands need OSBF_MODE_FAST: the exact mode's whole-image prefix is serial");
+    if (width < 1 || image_height < 1 || in_rows < 1 || out_rows < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "ImagePlane: dimensions must be >= 1");
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+    if (radius > osbf_gpu::kFastMaxRadius)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "fast mode supports radius <= %d (got %d)",
+                    osbf_gpu::kFastMaxRadius, radius);
+    if (out_row0 < 0 || out_row0 + out_rows > image_height)
+        return fail(OSBF_ERR_OUT_OF_RANGE, "output rows [%d, %d) outside the image height %d",
+                    out_row0, out_row0 + out_rows, image_height);
+    const int need0 = out_row0 - radius < 0 ? 0 : out_row0 - radius;
+    const int need1 = out_row0 + out_rows + radius > image_height ? image_height
+                                                                 : out_row0 + out_rows + radius;
+    if (in_row0 > need0 || in_row0 + in_rows < need1)
+        return fail(OSBF_ERR_OUT_OF_RANGE,
+                    "input rows [%d, %d) do not cover the band plus halo [%d, %d)", in_row0,
+                    in_row0 + in_rows, need0, need1);
+    if (!d_in || !d_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null plane pointer");
+    if (in_pitch < static_cast<size_t>(width) || out_pitch < static_cast<size_t>(width))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "pitch smaller than width");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    osbf_gpu::Geometry g{width, out_rows, 1};
+    g.img_height = image_height;
+    g.in_row0 = in_row0;
+    g.out_row0 = out_row0;
+    g.in_rows = in_rows;
+    const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_pitch * in_rows};
+    OSBF_CUDA(osbf_gpu::fast_step(input, g, radius, d_out, out_pitch, out_pitch * out_rows, nullptr,
+                                  nullptr, pick_stream(ctx, stream), ctx->lc),
+              "band step");
+    return OSBF_OK;
+}
+
 osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
                                double* h_out, int width, int height, int batch, int radius,
                                int iterations, osbf_mode mode) {

@@ -46,6 +46,17 @@ constexpr int NSB = NT / TW;    // Phase B row segments per column
 constexpr int SEGB = TH / NSB;  // rows per Phase B segment
 constexpr int kUnrollRadius = 4;  // full unroll (register ring) up to this radius
 
+// Rows of one launch in global image coordinates (see Geometry).
+struct Band {
+    int h_img;   // image height: windows clip at [0, h_img)
+    int y_in0;   // global row of input buffer row 0
+    int y_out0;  // global row of output buffer row 0 (first output row)
+    int y_end;   // one past the last output row (global)
+};
+inline Band band_of(const Geometry& g) {
+    return Band{g.img_h(), g.in_row0, g.out_row0, g.out_row0 + g.height};
+}
+
 template <int R>
 struct Lay {
     static constexpr int LH = TH + 2 * R;      // staged rows
@@ -77,14 +88,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Stage U rows [Y0-R, Y0+TH+R) x cols [X0-R, X0+TW+R), zero outside the image.
 template <int R, typename T, bool BORDER>
 __device__ __forceinline__ void stage_tile(const T* __restrict__ src, size_t pitch, int X0,
-                                           int Y0, int W, int H, double* __restrict__ Us) {
+                                           int Y0, int W, const Band& band,
+                                           double* __restrict__ Us) {
     using Ly = Lay<R>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int CHUNKS = (Ly::LWU + 31) / 32;
     for (int j = warp; j < Ly::LH; j += NT / 32) {
-        const int gy = Y0 - R + j;
-        const bool row_in = !BORDER || (gy >= 0 && gy < H);
-        const T* rowp = src + static_cast<size_t>(row_in ? gy : 0) * pitch;
+        const int gy = Y0 - R + j;  // global row; buffer row gy - y_in0
+        const bool row_in = !BORDER || (gy >= 0 && gy < band.h_img);
+        const T* rowp = src + static_cast<size_t>(row_in ? gy - band.y_in0 : 0) * pitch;
 #pragma unroll
         for (int c = 0; c < CHUNKS; ++c) {
             const int i = lane + 32 * c;
@@ -238,7 +250,8 @@ __device__ __forceinline__ void select_store(const double (&S)[8], double u, int
 template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
 __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
                                             const double* __restrict__ Hs, int X0, int Y0,
-                                            int W, int H, int b, double* __restrict__ outp,
+                                            int W, const Band& band, int b,
+                                            double* __restrict__ outp,
                                             size_t out_pitch, double* __restrict__ means,
                                             uint8_t* __restrict__ sel,
                                             const double* __restrict__ rtab) {
@@ -255,7 +268,8 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
     const double* f1 = Hs + y0 * Ly::PH + x;      // F1(j) = f1[j*PH]
     const double* f2 = Hs + y0 * Ly::PH + x + R;  // F2(j)
     const double* f3 = Us + y0 * Ly::PU + x + R;  // F3(j)
-    double* o = outp ? outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx : nullptr;
+    const int H = band.h_img;
+    double* o = outp ? outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx : nullptr;
 #define F1(j) f1[(j) * Ly::PH]
 #define F2(j) f2[(j) * Ly::PH]
 #define F3(j) f3[(j) * Ly::PU]
@@ -273,7 +287,7 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
             const int y = j - 2 * R;  // output row whose windows complete at row j
             if (y >= 0) {
                 const int gy = Y0 + y0 + y;
-                if (BORDER && gy >= H) break;
+                if (BORDER && gy >= band.y_end) break;
                 const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
                                      P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
                                      P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
@@ -311,7 +325,7 @@ __device__ __forceinline__ void column_walk(const double* __restrict__ Us,
                 u = n3;
             }
             const int gy = Y0 + y0 + y;
-            if (BORDER && gy >= H) break;
+            if (BORDER && gy >= band.y_end) break;
             const double S[8] = {dn1, dn2, up2, up1, up1 + dn1 - c1, up2 + dn2 - c2,
                                  dn1 + dn2 - dn3, up1 + up2 - up3};
             select_store<R, EXACT_DIV, BORDER, DIAG>(
@@ -331,31 +345,32 @@ template <int R, typename T, bool EXACT_DIV, bool DIAG>
 __global__ void __launch_bounds__(NT, Lay<R>::template min_ctas<EXACT_DIV || DIAG>())
     fast_sep_step(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
                   double* __restrict__ out, size_t out_pitch, size_t out_plane,
-                  double* __restrict__ means, uint8_t* __restrict__ sel, int W, int H) {
+                  double* __restrict__ means, uint8_t* __restrict__ sel, int W, Band band) {
     extern __shared__ double smem[];
     using Ly = Lay<R>;
     double* Us = smem;                   // [LH][PU]: tile row j <-> image row Y0 - R + j
     double* Hs = smem + Ly::LH * Ly::PU;  // [LH][PH]: Hs[j][k] = H(X0 + k, row j)
-    const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH, b = blockIdx.z;
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * TH, b = blockIdx.z;
     const T* src = in + static_cast<size_t>(b) * in_plane;
     double* outp = out ? out + static_cast<size_t>(b) * out_plane : nullptr;
     double* rtab = Hs + Ly::LH * Ly::PH;  // [NRT]: rtab[k] = 1/k
     if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
-    const bool interior = X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= H;
+    const bool interior = X0 >= R && X0 + TW + R <= W && Y0 >= R &&
+                          Y0 + TH + R <= band.h_img && Y0 + TH <= band.y_end;
     if (interior) {
-        stage_tile<R, T, false>(src, in_pitch, X0, Y0, W, H, Us);
+        stage_tile<R, T, false>(src, in_pitch, X0, Y0, W, band, Us);
     } else {
-        stage_tile<R, T, true>(src, in_pitch, X0, Y0, W, H, Us);
+        stage_tile<R, T, true>(src, in_pitch, X0, Y0, W, band, Us);
     }
     __syncthreads();
     arm_sums<R>(Us, Hs);
     __syncthreads();
     if (interior) {
-        column_walk<R, EXACT_DIV, false, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
-                                               sel, rtab);
+        column_walk<R, EXACT_DIV, false, DIAG>(Us, Hs, X0, Y0, W, band, b, outp, out_pitch,
+                                               means, sel, rtab);
     } else {
-        column_walk<R, EXACT_DIV, true, DIAG>(Us, Hs, X0, Y0, W, H, b, outp, out_pitch, means,
-                                              sel, rtab);
+        column_walk<R, EXACT_DIV, true, DIAG>(Us, Hs, X0, Y0, W, band, b, outp, out_pitch,
+                                              means, sel, rtab);
     }
 }
 
@@ -374,7 +389,7 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
     fast_sep_step<R, T, EXACT_DIV, DIAG><<<grid, NT, smem, s>>>(
         static_cast<const T*>(in.base), in.pitch, in.plane, out, op, opl, means, sel, g.width,
-        g.height);
+        band_of(g));
     return cudaGetLastError();
 }
 
@@ -407,7 +422,7 @@ struct TLay {
 
 template <int R, typename T, bool EXACT_DIV, bool BORDER>
 __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, int Y0, int W,
-                                            int H, int b, double* __restrict__ outp,
+                                            const Band& band, int b, double* __restrict__ outp,
                                             size_t out_pitch, const double* __restrict__ rtab) {
     using Ly = TLay<R, T>;
     const int x = threadIdx.x % TW, s = threadIdx.x / TW;
@@ -421,7 +436,8 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
     const int y0 = s * SEGB;
     // image (X0 + x + i - R, Y0 + y0 + j - R) = col[j*BW + i]
     const T* __restrict__ col = Us + y0 * Ly::BW + x + Ly::XOFF;
-    double* o = outp + static_cast<size_t>(Y0 + y0) * out_pitch + gx;
+    const int H = band.h_img;
+    double* o = outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
     constexpr int NJ = SEGB + 2 * R;
     double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
     P1[0] = P2[0] = Q[0] = 0.0;
@@ -444,7 +460,7 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
         const int y = j - 2 * R;
         if (y >= 0) {
             const int gy = Y0 + y0 + y;
-            if (BORDER && gy >= H) break;
+            if (BORDER && gy >= band.y_end) break;
             const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
                                  P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
                                  P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
@@ -459,27 +475,28 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
 template <int R, typename T, bool EXACT_DIV>
 __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3 : 2))
     fast_tma_step(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
-                  size_t out_pitch, size_t out_plane, int W, int H) {
+                  size_t out_pitch, size_t out_plane, int W, Band band) {
     using Ly = TLay<R, T>;
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ double rtab[Ly::NRT];
     const uint32_t base = tma::smem_u32(smem_raw);
     T* Us = reinterpret_cast<T*>(smem_raw + ((128u - (base & 127u)) & 127u));
-    const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH, b = blockIdx.z;
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * TH, b = blockIdx.z;
     if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
     if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
     __syncthreads();
     if (threadIdx.x == 0) {
         tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
-        tma::load_3d(Us, &tmap, X0 - Ly::RA, Y0 - R, b, &bar);
+        tma::load_3d(Us, &tmap, X0 - Ly::RA, Y0 - R - band.y_in0, b, &bar);
     }
     tma::mbar_wait(&bar, 0);
     double* outp = out + static_cast<size_t>(b) * out_plane;
-    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= H)
-        direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, H, b, outp, out_pitch, rtab);
+    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= band.h_img &&
+        Y0 + TH <= band.y_end)
+        direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
     else
-        direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, H, b, outp, out_pitch, rtab);
+        direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
 }
 
 template <typename T>
@@ -495,8 +512,8 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
                        size_t opl, cudaStream_t s) {
     using Ly = TLay<R, T>;
     CUtensorMap map;
-    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.height) * sizeof(T);
-    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.height, g.batch,
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
         return cudaErrorNotSupported;
     static bool configured = false;
@@ -508,7 +525,8 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
         configured = true;
     }
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
-    fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width, g.height);
+    fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                              band_of(g));
     return cudaGetLastError();
 }
 

@@ -20,8 +20,18 @@ struct PlaneView {
 
 struct Geometry {
     int width;
-    int height;
+    int height;  // output rows (the image height unless this is a row band)
     int batch;
+    // Row-band mode (one band of a taller image, fast mode only): the input
+    // buffer holds global rows [in_row0, in_row0 + in_rows), the output
+    // buffer global rows [out_row0, out_row0 + height); windows are clipped
+    // at the global image height img_height.  Defaults: the whole image.
+    int img_height = -1;
+    int in_row0 = 0;
+    int out_row0 = 0;
+    int in_rows = -1;
+    int img_h() const { return img_height < 0 ? height : img_height; }
+    int in_h() const { return in_rows < 0 ? height : in_rows; }
 };
 
 // Launch statistics (kernels issued) for instrumentation.

@@ -189,3 +189,50 @@ def test_in_place_and_pitched(ctx, oracle_lib):
     view = big[:, :96]  # pitched input (row stride 128)
     got = ctx.iterate(view, 3, 3, mode="exact")
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("r", [2, 7])
+def test_row_bands_equal_whole_image(ctx, r):
+    """osbf_gpu_step_band over 64-aligned row bands (halos copied from the
+    previous pass, as the multi-GPU exchange does) is bit-identical to the
+    whole-image fast pass; unaligned bands stay within the float tolerance."""
+    import torch
+
+    from paper_2108_05021_b200.dist import BandLayout
+
+    h, w, iters = 700, 300, 3
+    x = torch.from_numpy(np.random.default_rng(r).random((h, w))).cuda()
+    want = ctx.iterate(x, r, iters, mode="fast")
+    for world in (3, 4):
+        cur = x.clone()
+        for _ in range(iters):
+            nxt = torch.empty_like(cur)
+            for rank in range(world):
+                lay = BandLayout.make(h, w, r, world, rank)
+                src = cur[lay.buf_row0:lay.buf_row0 + lay.buf_rows].contiguous()
+                ctx.step_band(src, lay.buf_row0, nxt[lay.row0:lay.row1], lay.row0, lay.rows, h, r)
+            cur = nxt
+        assert torch.equal(cur.view(torch.int64), want.view(torch.int64)), world
+    # unaligned bands (tile grid shifted): same result within tolerance
+    cur = x.clone()
+    cuts = [0, 250, 333, 700]
+    for _ in range(iters):
+        nxt = torch.empty_like(cur)
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            b0, b1 = max(0, r0 - r), min(h, r1 + r)
+            ctx.step_band(cur[b0:b1].contiguous(), b0, nxt[r0:r1], r0, r1 - r0, h, r)
+        cur = nxt
+    assert float((cur - want).abs().max()) <= FLOAT_TOL
+
+
+def test_row_band_errors(ctx):
+    import torch
+
+    import paper_2108_05021_b200 as ob
+
+    x = torch.rand((64, 64), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(x)
+    with pytest.raises(ob.InvalidArgument):  # exact mode cannot be banded
+        ctx.step_band(x, 0, out, 0, 64, 64, 2, mode="exact")
+    with pytest.raises(ob.OutOfRange):  # halo missing
+        ctx.step_band(x[8:], 8, out[8:32], 8, 24, 64, 2)
