@@ -91,7 +91,7 @@ def exchange_halos(buf, lay: BandLayout, rank: int, world: int, group=None) -> N
     import torch.distributed as dist
 
     ops = []
-    top, r = lay.halo_top, lay.radius
+    top = lay.halo_top
     band = buf[top:top + lay.rows]
     if rank > 0 and lay.halo_top:
         ops.append(dist.P2POp(dist.isend, band[:lay.halo_top].contiguous(), rank - 1, group))
@@ -100,7 +100,6 @@ def exchange_halos(buf, lay: BandLayout, rank: int, world: int, group=None) -> N
         ops.append(dist.P2POp(dist.isend, band[lay.rows - lay.halo_bot:].contiguous(), rank + 1,
                               group))
         ops.append(dist.P2POp(dist.irecv, buf[top + lay.rows:], rank + 1, group))
-    del r
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -127,20 +126,28 @@ class RowBandOSBF:
         self._ctx.step_band(src, lay.buf_row0, dst_band, lay.row0, lay.rows, lay.height,
                             lay.radius, mode="fast")
 
-    def run(self, band, iterations: int):
-        """``band``: this rank's rows [row0, row1) (any float dtype, on the
-        compute device); returns the filtered band (float64)."""
+    def buffers(self, device):
+        """The two halo'd fp64 ping-pong buffers (allocated once, reused)."""
         import torch
 
         lay = self.lay
+        if getattr(self, "_bufs", None) is None or self._bufs[0].device != device:
+            self._bufs = [torch.zeros((lay.buf_rows, lay.width), dtype=torch.float64,
+                                      device=device) for _ in range(2)]
+        return self._bufs
+
+    def run(self, band, iterations: int):
+        """``band``: this rank's rows [row0, row1) (any float dtype, on the
+        compute device); returns the filtered band (a float64 view into the
+        rank's buffers, valid until the next run)."""
+        lay = self.lay
         if tuple(band.shape) != (lay.rows, lay.width):
             raise ValueError(f"band shape {tuple(band.shape)} != {(lay.rows, lay.width)}")
-        bufs = [torch.zeros((lay.buf_rows, lay.width), dtype=torch.float64, device=band.device)
-                for _ in range(2)]
+        bufs = self.buffers(band.device)
         top = lay.halo_top
         bufs[0][top:top + lay.rows].copy_(band)
         if iterations == 0:
-            return bufs[0][top:top + lay.rows].clone()
+            return bufs[0][top:top + lay.rows]
         exchange_halos(bufs[0], lay, self.rank, self.world, self.group)
         cur = 0
         for it in range(iterations):
