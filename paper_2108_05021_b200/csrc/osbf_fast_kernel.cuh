@@ -403,9 +403,16 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
 // run the prefix-sum walk.  The input is read in its own dtype (u8 / f32 /
 // f64) and promoted to fp64 in registers, so the first pass needs no
 // conversion kernel.
+// Radii with the TMA direct kernel.
+constexpr int kTmaRadius = 4;
+
 template <int R, typename T>
 struct TLay {
-    static constexpr int LH = TH + 2 * R;
+    // taller tiles for larger radii: (SEGT + 2R) / SEGT rows are touched per
+    // output row of a column segment
+    static constexpr int THT = R <= 2 ? 64 : 128;
+    static constexpr int SEGT = THT / NSB;
+    static constexpr int LH = THT + 2 * R;
     static constexpr int LWU = TW + 2 * R;
     // TMA needs 16-byte aligned box rows AND a 16-byte aligned innermost start
     // coordinate, so the box starts RA >= R columns left of the tile
@@ -433,12 +440,12 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
         const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
         cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
     }
-    const int y0 = s * SEGB;
+    const int y0 = s * Ly::SEGT;
     // image (X0 + x + i - R, Y0 + y0 + j - R) = col[j*BW + i]
     const T* __restrict__ col = Us + y0 * Ly::BW + x + Ly::XOFF;
     const int H = band.h_img;
     double* o = outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
-    constexpr int NJ = SEGB + 2 * R;
+    constexpr int NJ = Ly::SEGT + 2 * R;
     double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
     P1[0] = P2[0] = Q[0] = 0.0;
 #pragma unroll
@@ -473,7 +480,7 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
 }
 
 template <int R, typename T, bool EXACT_DIV>
-__global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3 : 2))
+__global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3 : (R <= 4 ? 2 : 1)))
     fast_tma_step(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
                   size_t out_pitch, size_t out_plane, int W, Band band) {
     using Ly = TLay<R, T>;
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3
     __shared__ double rtab[Ly::NRT];
     const uint32_t base = tma::smem_u32(smem_raw);
     T* Us = reinterpret_cast<T*>(smem_raw + ((128u - (base & 127u)) & 127u));
-    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * TH, b = blockIdx.z;
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * Ly::THT, b = blockIdx.z;
     if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
     if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
     __syncthreads();
@@ -492,8 +499,8 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3
     }
     tma::mbar_wait(&bar, 0);
     double* outp = out + static_cast<size_t>(b) * out_plane;
-    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + TH + R <= band.h_img &&
-        Y0 + TH <= band.y_end)
+    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
+        Y0 + Ly::THT <= band.y_end)
         direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
     else
         direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
@@ -524,7 +531,7 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    dim3 grid((g.width + TW - 1) / TW, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
     fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                               band_of(g));
     return cudaGetLastError();
@@ -533,7 +540,7 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
 template <int R, bool DIAG>
 cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, size_t op,
                          size_t opl, double* means, uint8_t* sel, cudaStream_t s) {
-    if constexpr (R <= kUnrollRadius && !DIAG) {
+    if constexpr (R <= kTmaRadius && !DIAG) {
         cudaError_t e = cudaErrorNotSupported;
         switch (in.dtype) {
             case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
