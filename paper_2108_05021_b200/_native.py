@@ -37,6 +37,7 @@ SIGNATURES = [
     ("osbf_gpu_ctx_destroy", _c_int, [_c_void_p]),
     ("osbf_gpu_ctx_trim", _c_int, [_c_void_p]),
     ("osbf_gpu_ctx_launch_count", ctypes.c_uint64, [_c_void_p]),
+    ("osbf_gpu_ctx_set_temporal_blocking", _c_int, [_c_void_p, _c_int]),
     ("osbf_gpu_iterate", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_void_p, _c_size, _c_size,
       _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),

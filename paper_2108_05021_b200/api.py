@@ -177,6 +177,10 @@ class Context:
     def launches(self) -> int:
         return int(self._lib.osbf_gpu_ctx_launch_count(self.handle))
 
+    def set_temporal_blocking(self, passes_per_launch: int) -> None:
+        """Fast mode: 2 = two passes per launch (radius <= 2), 1 = default."""
+        _check(self._lib.osbf_gpu_ctx_set_temporal_blocking(self.handle, passes_per_launch))
+
     # -- device tensors -----------------------------------------------------
     def iterate(self, src, radius: int, iterations: int, mode="exact", out=None, stream=None):
         """osbf over a CUDA tensor of shape (H, W) or (B, H, W), dtype uint8 /

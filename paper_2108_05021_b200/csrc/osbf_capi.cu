@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -77,6 +78,7 @@ struct osbf_ctx {
     DevBuf rowpfx, sat;        // exact-mode workspace
     DevBuf host_in, host_out;  // staging for the host entry points
     osbf_gpu::LaunchCounter lc;
+    int passes_per_launch = 1;  // fast mode temporal blocking: 1 or 2
 };
 
 namespace {
@@ -121,6 +123,16 @@ osbf_status check_mode(osbf_mode m) {
 // is ordered with e.g. PyTorch's default stream.  The context's own stream is
 // used only by the host-buffer entry points.
 cudaStream_t pick_stream(osbf_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
+
+// Temporal blocking (two fast passes per launch) is opt-in per context
+// (osbf_gpu_ctx_set_temporal_blocking) or process-wide with OSBF_GPU_TB2=1.
+bool tb2_env() {
+    static const bool on = [] {
+        const char* v = std::getenv("OSBF_GPU_TB2");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
 
 // One pass in the requested mode: src (typed view) -> dst (fp64).
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
@@ -247,6 +259,14 @@ osbf_status osbf_gpu_ctx_trim(osbf_ctx* ctx) {
 
 uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx) { return ctx ? ctx->lc.launches : 0; }
 
+osbf_status osbf_gpu_ctx_set_temporal_blocking(osbf_ctx* ctx, int passes_per_launch) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (passes_per_launch != 1 && passes_per_launch != 2)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "passes_per_launch must be 1 or 2");
+    ctx->passes_per_launch = passes_per_launch;
+    return OSBF_OK;
+}
+
 osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
                              size_t in_pitch, size_t in_plane_stride, double* d_out,
                              size_t out_pitch, size_t out_plane_stride, int width, int height,
@@ -284,23 +304,42 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
     if (scratch_needed > 0) OSBF_CUDA(ctx->ping.ensure(plane * batch * sizeof(double)), "alloc ping");
     if (scratch_needed > 1) OSBF_CUDA(ctx->pong.ensure(plane * batch * sizeof(double)), "alloc pong");
     osbf_gpu::PlaneView src = input;
-    for (int it = 0; it < iterations; ++it) {
-        const bool last = it == iterations - 1;
-        double* dst;
-        size_t dp, dpl;
-        if (last && !alias) {
-            dst = d_out;
-            dp = out_pitch;
-            dpl = out_plane_stride;
-        } else {
-            DevBuf& buf = (it % 2 == 0) ? ctx->ping : ctx->pong;
-            dst = buf.as<double>();
-            dp = width;
-            dpl = plane;
+    int done = 0;
+    for (int step = 0; done < iterations; ++step) {
+        // Fast mode runs two passes per launch (temporal blocking) when the
+        // radius has a two-pass kernel; otherwise one pass per launch.
+        const bool tb2 = ctx->passes_per_launch == 2 || tb2_env();
+        int npass = (mode == OSBF_MODE_FAST && iterations - done >= 2 && tb2) ? 2 : 1;
+        for (;;) {
+            const bool last = done + npass == iterations;
+            double* dst;
+            size_t dp, dpl;
+            if (last && !alias) {
+                dst = d_out;
+                dp = out_pitch;
+                dpl = out_plane_stride;
+            } else {
+                DevBuf& buf = (step % 2 == 0) ? ctx->ping : ctx->pong;
+                dst = buf.as<double>();
+                dp = width;
+                dpl = plane;
+            }
+            if (npass == 2) {
+                const cudaError_t e = osbf_gpu::fast_step2(src, g, radius, dst, dp, dpl, s, ctx->lc);
+                if (e == cudaErrorNotSupported) {
+                    cudaGetLastError();
+                    npass = 1;
+                    continue;
+                }
+                OSBF_CUDA(e, "fast two-pass step");
+            } else if ((st = one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s)) !=
+                       OSBF_OK) {
+                return st;
+            }
+            src = osbf_gpu::PlaneView{dst, OSBF_F64, dp, dpl};
+            done += npass;
+            break;
         }
-        if ((st = one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s)) != OSBF_OK)
-            return st;
-        src = osbf_gpu::PlaneView{dst, OSBF_F64, dp, dpl};
     }
     if (alias) {
         OSBF_CUDA(cudaMemcpy2DAsync(d_out, out_pitch * sizeof(double), src.base,

@@ -403,8 +403,10 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
 // run the prefix-sum walk.  The input is read in its own dtype (u8 / f32 /
 // f64) and promoted to fp64 in registers, so the first pass needs no
 // conversion kernel.
-// Radii with the TMA direct kernel.
+// Radii with the TMA direct kernel, and with the two-pass (temporally
+// blocked) kernel.
 constexpr int kTmaRadius = 4;
+constexpr int kTb2Radius = 2;
 
 template <int R, typename T>
 struct TLay {
@@ -570,6 +572,210 @@ cudaError_t fast_launch_radius(const PlaneView& in, const Geometry& g, double* o
     if (means || sel)
         return fastk::launch_dtype<R, true>(in, g, out, out_pitch, out_plane, means, sel, s);
     return fastk::launch_dtype<R, false>(in, g, out, out_pitch, out_plane, means, sel, s);
+}
+
+}  // namespace osbf_gpu
+
+// ===========================================================================
+// Temporal blocking: two OSBF passes per HBM round trip (north-star K4).
+//
+// The tile is staged with a 2R halo; pass 1 computes the intermediate plane
+// over the output tile plus an R halo into shared memory (exactly what a
+// separate pass would write to HBM: clipped counts at the global border,
+// zero outside the image so pass 2's sums see the same zero fill); pass 2
+// computes the output tile from it.  HBM traffic per iteration halves; the
+// extra work is the R-wide ring of intermediate pixels ((TW+2R)(TH+2R)/TW/TH).
+namespace osbf_gpu {
+namespace fastk {
+
+template <int R, typename T>
+struct TB2Lay {
+    static constexpr int IW = TW + 2 * R;  // intermediate columns: [X0-R, X0+TW+R)
+    static constexpr int IH = TH + 2 * R;  // intermediate rows
+    static constexpr int IP = IW;          // intermediate pitch (doubles)
+    static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
+    static constexpr int RA2 = (2 * R + ALIGN - 1) / ALIGN * ALIGN;  // aligned 2R halo
+    static constexpr int XOFF = RA2 - 2 * R;
+    static constexpr int BW = (TW + RA2 + 2 * R + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int LH = TH + 4 * R;
+    static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
+    static constexpr int NSEG1 = 4, NSEG2 = 4;
+    static constexpr int SEG1 = (IH + NSEG1 - 1) / NSEG1;  // pass-1 rows per segment
+    static constexpr int SEG2 = TH / NSEG2;
+    static constexpr int NT1 = IW * NSEG1, NT2 = TW * NSEG2;
+    static constexpr int NTT = ((NT1 > NT2 ? NT1 : NT2) + 31) / 32 * 32;
+    static constexpr int NRT = 2 * R + 2;
+    static constexpr size_t I_BYTES = sizeof(double) * static_cast<size_t>(IH) * IP;
+    static constexpr size_t SMEM = 128 + ((TILE_BYTES + 15) / 16) * 16 + I_BYTES;
+};
+
+// One column walk (prefix-sum formulation, see direct_walk): source rows
+// src[j*pitch + i], j in [0, nrows + 2R), i in [0, 2R]; outputs for rows
+// [0, nrows) at global (gx, gy0 + y).  TO_SMEM: write to dst[y*dst_pitch]
+// with 0 for positions outside the image; else to global memory.
+template <int R, typename S, bool EXACT_DIV, bool BORDER, bool TO_SMEM, int NSEG>
+__device__ __forceinline__ void tb_walk(const S* __restrict__ col, int pitch, int nrows, int gx,
+                                        int gy0, int W, const Band& band, double* __restrict__ o,
+                                        size_t o_pitch, const double* __restrict__ rtab) {
+    const int H = band.h_img;
+    const bool col_in = gx >= 0 && gx < W;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (BORDER && col_in) {
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    constexpr int NJ = NSEG + 2 * R;
+    double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
+    P1[0] = P2[0] = Q[0] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        double v[2 * R + 1];
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) v[i] = to_f64(col[j * pitch + i]);
+        double a = v[0], c = v[R];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) {
+            a += v[i];
+            c += v[R + i];
+        }
+        const double e = v[R];
+        Uc[j] = e;
+        P1[j + 1] = P1[j] + a;
+        P2[j + 1] = P2[j] + c;
+        Q[j + 1] = Q[j] + ((a + c) - e);
+        const int y = j - 2 * R;
+        if (y >= 0 && y < nrows) {
+            const int gy = gy0 + y;
+            if (TO_SMEM) {
+                if (!BORDER || (col_in && gy >= 0 && gy < H)) {
+                    const double S8[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                          P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                          P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                          Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+                    select_store<R, EXACT_DIV, BORDER, false>(S8, Uc[y + R], gx, gy, W, H, 0, o,
+                                                              nullptr, nullptr, cf, rtab);
+                } else {
+                    *o = 0.0;
+                }
+            } else {
+                if (BORDER && gy >= band.y_end) break;
+                const double S8[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                      P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                      P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                      Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+                select_store<R, EXACT_DIV, BORDER, false>(S8, Uc[y + R], gx, gy, W, H, 0, o,
+                                                          nullptr, nullptr, cf, rtab);
+            }
+            o += o_pitch;
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT1>
+__global__ void __launch_bounds__(TB2Lay<R, T>::NTT, 2)
+    fast_tma_step2(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+                   size_t out_pitch, size_t out_plane, int W, Band band) {
+    using Ly = TB2Lay<R, T>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ double rtab[Ly::NRT];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    unsigned char* aligned = smem_raw + ((128u - (base & 127u)) & 127u);
+    T* Us = reinterpret_cast<T*>(aligned);
+    double* Is = reinterpret_cast<double*>(aligned + ((Ly::TILE_BYTES + 15) / 16) * 16);
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * TH, b = blockIdx.z;
+    const int tid = threadIdx.x;
+    if (tid == 0) tma::mbar_init(&bar, 1);
+    if (tid < Ly::NRT) rtab[tid] = tid ? 1.0 / tid : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+        tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
+        tma::load_3d(Us, &tmap, X0 - Ly::RA2, Y0 - 2 * R - band.y_in0, b, &bar);
+    }
+    tma::mbar_wait(&bar, 0);
+    // interior: every intermediate and output position inside the image
+    const bool interior = X0 >= 2 * R && X0 + TW + 2 * R <= W && Y0 >= 2 * R &&
+                          Y0 + TH + 2 * R <= band.h_img && Y0 + TH <= band.y_end;
+    // ---- pass 1: intermediate rows [Y0-R, Y0+TH+R), cols [X0-R, X0+TW+R)
+    if (tid < Ly::NT1) {
+        const int xi = tid % Ly::IW, s = tid / Ly::IW;
+        const int yi0 = s * Ly::SEG1;
+        const int nrows = min(Ly::SEG1, Ly::IH - yi0);
+        if (nrows > 0) {
+            const T* col = Us + yi0 * Ly::BW + xi + Ly::XOFF;
+            double* o = Is + yi0 * Ly::IP + xi;
+            const int gx = X0 - R + xi, gy0 = Y0 - R + yi0;
+            if (interior)
+                tb_walk<R, T, EXACT1, false, true, Ly::SEG1>(col, Ly::BW, nrows, gx, gy0, W, band,
+                                                             o, Ly::IP, rtab);
+            else
+                tb_walk<R, T, EXACT1, true, true, Ly::SEG1>(col, Ly::BW, nrows, gx, gy0, W, band,
+                                                            o, Ly::IP, rtab);
+        }
+    }
+    __syncthreads();
+    // ---- pass 2: output tile from the intermediate
+    if (tid < Ly::NT2) {
+        const int x = tid % TW, s = tid / TW;
+        const int gx = X0 + x;
+        if (interior || gx < W) {
+            const int y0 = s * Ly::SEG2;
+            const double* col = Is + y0 * Ly::IP + x;
+            double* o = out + static_cast<size_t>(b) * out_plane +
+                        static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
+            if (interior)
+                tb_walk<R, double, false, false, false, Ly::SEG2>(col, Ly::IP, Ly::SEG2, gx,
+                                                                  Y0 + y0, W, band, o, out_pitch,
+                                                                  rtab);
+            else
+                tb_walk<R, double, false, true, false, Ly::SEG2>(col, Ly::IP, Ly::SEG2, gx,
+                                                                 Y0 + y0, W, band, o, out_pitch,
+                                                                 rtab);
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT1>
+cudaError_t launch_tma2(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                        size_t opl, cudaStream_t s) {
+    using Ly = TB2Lay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+        return cudaErrorNotSupported;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_tma_step2<R, T, EXACT1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Ly::SMEM));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    fast_tma_step2<R, T, EXACT1><<<grid, Ly::NTT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                                 band_of(g));
+    return cudaGetLastError();
+}
+
+}  // namespace fastk
+
+// Two passes in one launch (radius <= kTb2Radius); cudaErrorNotSupported
+// when not applicable (caller falls back to two single passes).
+template <int R>
+cudaError_t fast_launch_radius2(const PlaneView& in, const Geometry& g, double* out,
+                                size_t out_pitch, size_t out_plane, cudaStream_t s) {
+    if constexpr (R <= fastk::kTb2Radius) {
+        switch (in.dtype) {
+            case OSBF_U8:
+                return fastk::launch_tma2<R, uint8_t, true>(in, g, out, out_pitch, out_plane, s);
+            case OSBF_F32:
+                return fastk::launch_tma2<R, float, false>(in, g, out, out_pitch, out_plane, s);
+            default:
+                return fastk::launch_tma2<R, double, false>(in, g, out, out_pitch, out_plane, s);
+        }
+    }
+    return cudaErrorNotSupported;
 }
 
 }  // namespace osbf_gpu

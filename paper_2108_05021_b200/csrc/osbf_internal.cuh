@@ -69,6 +69,12 @@ cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double
                       size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
                       cudaStream_t s, LaunchCounter& lc);
 
+// Two fast passes in one launch (temporal blocking).  Returns
+// cudaErrorNotSupported (nothing launched) when the radius / layout has no
+// two-pass kernel; the caller then runs two single passes.
+cudaError_t fast_step2(const PlaneView& in, const Geometry& g, int radius, double* out,
+                       size_t out_pitch, size_t out_plane, cudaStream_t s, LaunchCounter& lc);
+
 // ---- utilities (osbf_capi.cu) ----------------------------------------------
 cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t out_pitch,
                            size_t out_plane, cudaStream_t s, LaunchCounter& lc);
