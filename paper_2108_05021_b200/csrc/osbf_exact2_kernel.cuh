@@ -82,8 +82,11 @@ struct XLay {
     // table rows kept: [y0-BR-R, y0+BR] (2BR+R+1 rows), as a power of two
     static constexpr int NRING = (2 * BR + R + 2) <= 128 ? 128 : 256;
     static constexpr int U_ELEMS = BR * PUB;
+    // row segments of SW columns between stored carries (RR parallelism)
+    static constexpr int NSEGR = (NU + SW - 1) / SW;
+    static_assert(NSEGR * BR <= NT, "row segments exceed the CTA");
     static constexpr size_t SMEM =
-        sizeof(double) * (3 * static_cast<size_t>(U_ELEMS) + BR * PR + NRING * NCC + 2 * BR);
+        sizeof(double) * (3 * static_cast<size_t>(U_ELEMS) + BR * PR + NRING * NCC + 2 * BR * NSEGR);
 };
 
 }  // namespace ex2
@@ -215,9 +218,11 @@ __device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pi
             }
         }
     }
-    if (threadIdx.x < BR) {
-        const int y = y0 + threadIdx.x;
-        cs[threadIdx.x] = y < H ? carries[(gbase + y) * nsc + s0] : 0.0;
+    // carries R(xs + 16*seg - 1, y) for the row segments (cs[seg*BR + row])
+    if (threadIdx.x < BR * L::NSEGR) {
+        const int rr = threadIdx.x % BR, seg = threadIdx.x / BR;
+        const int y = y0 + rr;
+        cs[threadIdx.x] = (y < H && s0 + seg < nsc) ? carries[(gbase + y) * nsc + s0 + seg] : 0.0;
     }
     cp_commit();
 }
@@ -264,17 +269,42 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
             // (ca, cb, ra, rb) per window in reference order (core.hpp:212-225)
             constexpr int W8[8][4] = {{0, 2, 1, 3}, {1, 3, 1, 3}, {1, 3, 0, 2}, {0, 2, 0, 2},
                                       {0, 2, 0, 3}, {1, 3, 0, 3}, {0, 3, 1, 3}, {0, 3, 0, 2}};
+            double av[8], dv[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int ca = W8[i][0], cb = W8[i][1], ra = W8[i][2], rb = W8[i][3];
                 const double s =
                     __dadd_rn(__dsub_rn(__dsub_rn(g[rb][cb], g[rb][ca]), g[ra][cb]), g[ra][ca]);
-                const double a = SAFE ? div_by_count_unguarded(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh)
-                                      : div_by_count(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh);
-                const double d = fabs(__dsub_rn(a, u));
-                if (d < best_abs) {
-                    best_abs = d;
-                    best = a;
+                av[i] = SAFE ? div_by_count_unguarded(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh)
+                             : div_by_count(s, i < 4 ? kNq : kNh, i < 4 ? kYq : kYh);
+                dv[i] = fabs(__dsub_rn(av[i], u));
+            }
+            // With every |a_i - u| finite, "first i with the smallest d_i"
+            // (strict <, filters2d.hpp:78) is what a stable depth-3 tournament
+            // returns; non-finite pixels (NaN/inf input) keep the sequential
+            // rule, under which such windows are never selected.
+            const double dsum = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
+            if (fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL)) {
+                auto pick = [](double& d0, double& a0, double d1, double a1) {
+                    const bool t = d1 < d0;
+                    d0 = t ? d1 : d0;
+                    a0 = t ? a1 : a0;
+                };
+                pick(dv[0], av[0], dv[1], av[1]);
+                pick(dv[2], av[2], dv[3], av[3]);
+                pick(dv[4], av[4], dv[5], av[5]);
+                pick(dv[6], av[6], dv[7], av[7]);
+                pick(dv[0], av[0], dv[2], av[2]);
+                pick(dv[4], av[4], dv[6], av[6]);
+                pick(dv[0], av[0], dv[4], av[4]);
+                best = av[0];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (dv[i] < best_abs) {
+                        best_abs = dv[i];
+                        best = av[i];
+                    }
                 }
             }
         } else {
@@ -302,7 +332,7 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
 }
 
 template <int R, typename T>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, 2)
     exact_strip(const T* __restrict__ in, size_t pitch, size_t plane,
                 const double* __restrict__ carries, int nsc, double* __restrict__ out,
                 size_t opitch, size_t oplane, int W, int H) {
@@ -311,7 +341,7 @@ __global__ void __launch_bounds__(NT, 1)
     double* Ubuf = sm;                          // 3 x [BR][PUB]
     double* Rb = sm + 3 * L::U_ELEMS;           // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
     double* Cr = Rb + BR * L::PR;               // [NRING][NCC]: table rows, column cx = X0-R+t
-    double* cs = Cr + L::NRING * L::NCC;        // 2 x [BR] staged carries
+    double* cs = Cr + L::NRING * L::NCC;        // 2 x [NSEGR][BR] staged carries
     const int b = blockIdx.y;
     const int X0 = blockIdx.x * TW;
     const int xs_raw = X0 - R;
@@ -335,24 +365,35 @@ __global__ void __launch_bounds__(NT, 1)
         const int nrows = min(BR, H - y0);
         if (k + 1 < nblocks)
             stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + BR, W, H,
-                              Ubuf + ((k + 1) % 3) * L::U_ELEMS, cs + ((k + 1) & 1) * BR,
+                              Ubuf + ((k + 1) % 3) * L::U_ELEMS, cs + ((k + 1) & 1) * BR * L::NSEGR,
                               aligned16);
         else
             cp_commit();
         cp_wait<1>();
         __syncthreads();
-        // RR: continue the row running sums from the stored carries.
-        if (tid < BR) {
-            const double* u = Ubuf + (k % 3) * L::U_ELEMS + tid * L::PUB;
-            double* rb = Rb + tid * L::PR;
-            const int jfirst = xs - 1 - (X0 - R - 1);
-            for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;  // x < -1 (strip 0)
-            double acc = cs[(k & 1) * BR + tid];  // R(xs - 1)
-            if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = acc;
-            for (int x = xs; x <= xe; ++x) {
-                acc = __dadd_rn(acc, u[x - xs]);
-                const int j = x - (X0 - R - 1);
-                if (j >= 0) rb[j] = acc;
+        // RR: continue the row running sums from the stored carries, one
+        // SW-column segment per thread (every segment starts from the exact
+        // carry K1 stored, so the adds are the reference's serial chain).
+        if (tid < BR * L::NSEGR) {
+            const int rr = tid % BR, seg = tid / BR;
+            const double* u = Ubuf + (k % 3) * L::U_ELEMS + rr * L::PUB;
+            double* rb = Rb + rr * L::PR;
+            const int jbase = X0 - R - 1;  // x of Rb[0]
+            if (seg == 0) {
+                const int jfirst = xs - 1 - jbase;
+                for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;  // x < -1 (strip 0)
+                if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = cs[(k & 1) * BR * L::NSEGR + rr];
+            }
+            const int xa = xs + seg * SW;
+            double acc = cs[(k & 1) * BR * L::NSEGR + seg * BR + rr];  // R(xa - 1)
+#pragma unroll
+            for (int i = 0; i < SW; ++i) {
+                const int x = xa + i;
+                if (x <= xe) {
+                    acc = __dadd_rn(acc, u[seg * SW + i]);  // row += src[x]
+                    const int j = x - jbase;
+                    if (j >= 0 && j < L::NCC) rb[j] = acc;
+                }
             }
         }
         __syncthreads();
