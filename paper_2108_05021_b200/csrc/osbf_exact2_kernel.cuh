@@ -85,8 +85,17 @@ struct XLay {
     // row segments of SW columns between stored carries (RR parallelism)
     static constexpr int NSEGR = (NU + SW - 1) / SW;
     static_assert(NSEGR * BR <= NT, "row segments exceed the CTA");
-    static constexpr size_t SMEM =
-        sizeof(double) * (3 * static_cast<size_t>(U_ELEMS) + BR * PR + NRING * NCC + 2 * BR * NSEGR);
+    // U buffers in flight: S(k-1), block k, RR(k+1); block k+2 is staged
+    // into S(k-1)'s buffer after iteration k's last barrier
+    static constexpr int NUB = 3;
+    static constexpr size_t SMEM = sizeof(double) * (NUB * static_cast<size_t>(U_ELEMS) + BR * PR +
+                                                     NRING * NCC + 2 * BR * NSEGR);
+    // warps: column chains on [0, CCW), the early stencil rows on the rest;
+    // row prefixes on [0, RRW), the late stencil rows on the rest
+    static constexpr int CCW = (NCC + 31) / 32;
+    static constexpr int RRW = (NSEGR * BR + 31) / 32;
+    static_assert(CCW < NT / 32 && RRW < NT / 32, "no warps left for the stencil");
+    static_assert(2 * BR + R + 1 <= NRING, "table ring too small");
 };
 
 }  // namespace ex2
@@ -237,20 +246,20 @@ __device__ __forceinline__ int ring_row(int cy) {
 template <int R, bool SAFE>
 __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
                                              const double* __restrict__ U, int xs, int X0, int yb,
-                                             int nrows, int W, int H, double* __restrict__ outp,
-                                             size_t opitch) {
+                                             int r_lo, int r_hi, int w_first, int n_w, int W,
+                                             int H, double* __restrict__ outp, size_t opitch) {
     using L = XLay<R>;
-    const int lx = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int lx = threadIdx.x & 31, grp = (threadIdx.x >> 5) - w_first;
     const int x = X0 + lx;
-    if (x >= W) return;
+    if (x >= W || grp < 0 || grp >= n_w) return;
     const int cbase = X0 - R;  // table column of Cr index 0
     constexpr double kYq = 1.0 / ((R + 1) * (R + 1));
     constexpr double kYh = 1.0 / ((R + 1) * (2 * R + 1));
     constexpr double kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
     const bool col_int = x >= R && x + R < W;
-    double* op = outp + static_cast<size_t>(yb + grp) * opitch + x;
-    const size_t ostep = static_cast<size_t>(NT / 32) * opitch;
-    for (int rr = grp; rr < nrows; rr += NT / 32, op += ostep) {
+    double* op = outp + static_cast<size_t>(yb + r_lo + grp) * opitch + x;
+    const size_t ostep = static_cast<size_t>(n_w) * opitch;
+    for (int rr = r_lo + grp; rr < r_hi; rr += n_w, op += ostep) {
         const int y = yb + rr;
         const double u = U[rr * L::PUB + (x - xs)];
         double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
@@ -338,8 +347,8 @@ __global__ void __launch_bounds__(NT, 2)
                 size_t opitch, size_t oplane, int W, int H) {
     using L = XLay<R>;
     extern __shared__ double sm[];
-    double* Ubuf = sm;                          // 3 x [BR][PUB]
-    double* Rb = sm + 3 * L::U_ELEMS;           // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
+    double* Ubuf = sm;                          // NUB x [BR][PUB]
+    double* Rb = sm + L::NUB * L::U_ELEMS;      // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
     double* Cr = Rb + BR * L::PR;               // [NRING][NCC]: table rows, column cx = X0-R+t
     double* cs = Cr + L::NRING * L::NCC;        // 2 x [NSEGR][BR] staged carries
     const int b = blockIdx.y;
@@ -356,78 +365,104 @@ __global__ void __launch_bounds__(NT, 2)
 
     double creg = 0.0;    // running table column (threads < NCC)
     bool unsafe = false;  // some table value outside the unguarded-division range
-    if (tid < L::NCC) Cr[ring_row<R>(0) * L::NCC + tid] = 0.0;  // zero border row
+    const int warp = tid >> 5;
     const bool aligned16 = sizeof(T) == 8 && (pitch % 2 == 0) &&
                            (reinterpret_cast<uintptr_t>(src) % 16 == 0);
-    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, 0, W, H, Ubuf, cs, aligned16);
+    auto U_of = [&](int k) { return Ubuf + (k % L::NUB) * L::U_ELEMS; };
+    auto cs_of = [&](int k) { return cs + (k & 1) * BR * L::NSEGR; };
+
+    // RR: continue the row running sums of block k from the stored carries,
+    // one SW-column segment per thread (each segment starts from the exact
+    // carry K1 stored, so the adds are the reference's serial chain).
+    auto row_prefix = [&](int k) {
+        if (tid >= BR * L::NSEGR) return;
+        const int rr = tid % BR, seg = tid / BR;
+        const double* u = U_of(k) + rr * L::PUB;
+        const double* c = cs_of(k);
+        double* rb = Rb + rr * L::PR;
+        const int jbase = X0 - R - 1;  // x of Rb[0]
+        if (seg == 0) {
+            const int jfirst = xs - 1 - jbase;
+            for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;  // x < -1 (strip 0)
+            if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = c[rr];
+        }
+        const int xa = xs + seg * SW;
+        double acc = c[seg * BR + rr];  // R(xa - 1)
+#pragma unroll
+        for (int i = 0; i < SW; ++i) {
+            const int x = xa + i;
+            if (x <= xe) {
+                acc = __dadd_rn(acc, u[seg * SW + i]);  // row += src[x]
+                const int j = x - jbase;
+                if (j >= 0 && j < L::NCC) rb[j] = acc;
+            }
+        }
+    };
+
+    if (tid < L::NCC) Cr[ring_row<R>(0) * L::NCC + tid] = 0.0;  // zero border row
+    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, 0, W, H, U_of(0), cs_of(0),
+                      aligned16);
+    cp_wait<0>();
+    __syncthreads();
+    if (nblocks > 1)  // lands during iteration 0's phase A
+        stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, BR, W, H, U_of(1), cs_of(1),
+                          aligned16);
+    row_prefix(0);
+    __syncthreads();
+    const int early = BR - R - 1 > 0 ? BR - R - 1 : 0;  // rows of block k-1 not needing block k
     for (int k = 0; k < nblocks; ++k) {
         const int y0 = k * BR;
         const int nrows = min(BR, H - y0);
-        if (k + 1 < nblocks)
-            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + BR, W, H,
-                              Ubuf + ((k + 1) % 3) * L::U_ELEMS, cs + ((k + 1) & 1) * BR * L::NSEGR,
-                              aligned16);
-        else
-            cp_commit();
-        cp_wait<1>();
-        __syncthreads();
-        // RR: continue the row running sums from the stored carries, one
-        // SW-column segment per thread (every segment starts from the exact
-        // carry K1 stored, so the adds are the reference's serial chain).
-        if (tid < BR * L::NSEGR) {
-            const int rr = tid % BR, seg = tid / BR;
-            const double* u = Ubuf + (k % 3) * L::U_ELEMS + rr * L::PUB;
-            double* rb = Rb + rr * L::PR;
-            const int jbase = X0 - R - 1;  // x of Rb[0]
-            if (seg == 0) {
-                const int jfirst = xs - 1 - jbase;
-                for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;  // x < -1 (strip 0)
-                if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = cs[(k & 1) * BR * L::NSEGR + rr];
-            }
-            const int xa = xs + seg * SW;
-            double acc = cs[(k & 1) * BR * L::NSEGR + seg * BR + rr];  // R(xa - 1)
-#pragma unroll
-            for (int i = 0; i < SW; ++i) {
-                const int x = xa + i;
-                if (x <= xe) {
-                    acc = __dadd_rn(acc, u[seg * SW + i]);  // row += src[x]
-                    const int j = x - jbase;
-                    if (j >= 0 && j < L::NCC) rb[j] = acc;
+        // Phase A: table columns of block k  ||  rows of block k-1 whose
+        // windows end before block k's table rows (all but the last R+1)
+        const bool safe_prev = !unsafe;
+        if (warp < L::CCW) {
+            bool unsafe_here = false;
+            if (tid < L::NCC) {
+                const int cx = X0 - R + tid;
+                if (cx >= 0 && cx <= W) {
+                    for (int rr = 0; rr < nrows; ++rr) {
+                        creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);  // above[x+1] + row
+                        unsafe_here |= !table_value_safe(creg);
+                        Cr[ring_row<R>(y0 + rr + 1) * L::NCC + tid] = creg;
+                    }
                 }
             }
-        }
-        __syncthreads();
-        // CC: continue the table columns down the block.
-        bool unsafe_here = false;
-        if (tid < L::NCC) {
-            const int cx = X0 - R + tid;
-            if (cx >= 0 && cx <= W) {
-                for (int rr = 0; rr < nrows; ++rr) {
-                    creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);  // above[x+1] + row
-                    unsafe_here |= !table_value_safe(creg);
-                    Cr[ring_row<R>(y0 + rr + 1) * L::NCC + tid] = creg;
-                }
-            }
-        }
-        unsafe = __syncthreads_or(unsafe || unsafe_here);  // sticky for the strip
-        // S: previous block's rows now have every table row they need.
-        if (k > 0) {
-            if (!unsafe)
-                stencil_rows<R, true>(Cr, Ubuf + ((k - 1) % 3) * L::U_ELEMS, xs, X0, y0 - BR, BR,
-                                      W, H, outp, opitch);
+            unsafe |= unsafe_here;
+        } else if (k > 0) {
+            if (safe_prev)
+                stencil_rows<R, true>(Cr, U_of(k - 1), xs, X0, y0 - BR, 0, early, L::CCW,
+                                      NT / 32 - L::CCW, W, H, outp, opitch);
             else
-                stencil_rows<R, false>(Cr, Ubuf + ((k - 1) % 3) * L::U_ELEMS, xs, X0, y0 - BR, BR,
-                                       W, H, outp, opitch);
+                stencil_rows<R, false>(Cr, U_of(k - 1), xs, X0, y0 - BR, 0, early, L::CCW,
+                                       NT / 32 - L::CCW, W, H, outp, opitch);
+        }
+        cp_wait<0>();  // block k+1 staged
+        unsafe = __syncthreads_or(unsafe);  // sticky for the strip
+        // Phase B: row prefixes of block k+1  ||  the last R+1 rows of block k-1
+        if (warp < L::RRW) {
+            if (k + 1 < nblocks) row_prefix(k + 1);
+        } else if (k > 0) {
+            if (!unsafe)
+                stencil_rows<R, true>(Cr, U_of(k - 1), xs, X0, y0 - BR, early, BR, L::RRW,
+                                      NT / 32 - L::RRW, W, H, outp, opitch);
+            else
+                stencil_rows<R, false>(Cr, U_of(k - 1), xs, X0, y0 - BR, early, BR, L::RRW,
+                                       NT / 32 - L::RRW, W, H, outp, opitch);
         }
         __syncthreads();
+        // block k+2 into the buffer S(k-1) just released; lands during k+1
+        if (k + 2 < nblocks)
+            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + 2 * BR, W, H,
+                              U_of(k + 2), cs_of(k + 2), aligned16);
     }
     const int ylast = (nblocks - 1) * BR;
     if (!unsafe)
-        stencil_rows<R, true>(Cr, Ubuf + ((nblocks - 1) % 3) * L::U_ELEMS, xs, X0, ylast,
-                              H - ylast, W, H, outp, opitch);
+        stencil_rows<R, true>(Cr, U_of(nblocks - 1), xs, X0, ylast, 0, H - ylast, 0, NT / 32, W,
+                              H, outp, opitch);
     else
-        stencil_rows<R, false>(Cr, Ubuf + ((nblocks - 1) % 3) * L::U_ELEMS, xs, X0, ylast,
-                               H - ylast, W, H, outp, opitch);
+        stencil_rows<R, false>(Cr, U_of(nblocks - 1), xs, X0, ylast, 0, H - ylast, 0, NT / 32, W,
+                               H, outp, opitch);
 }
 
 }  // namespace ex2
