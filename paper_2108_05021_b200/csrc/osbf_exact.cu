@@ -194,7 +194,7 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
 
 namespace {
 using Exact2Fn = cudaError_t (*)(const PlaneView&, const Geometry&, double*, int, double*, size_t,
-                                 size_t, cudaStream_t);
+                                 size_t, int, double*, cudaStream_t);
 constexpr Exact2Fn kExact2[kExactFusedMaxRadius + 1] = {
     nullptr,
     exact2_launch_radius<1>,  exact2_launch_radius<2>,  exact2_launch_radius<3>,
@@ -225,8 +225,31 @@ cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carri
 }
 }  // namespace
 
+// Band height for under-occupied launches (few strips x planes): enough
+// bands for ~4 CTAs per SM, each at least 128 rows (it re-walks 2 blocks).
+int exact_band_height(const Geometry& g) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const long long ctas = static_cast<long long>((g.width + ex2::TW - 1) / ex2::TW) * g.batch;
+    const long long want = 4LL * sms;
+    if (ctas >= want / 2 || g.height < 4 * 128) return 0;
+    long long nb = (want + ctas - 1) / ctas;
+    int bh = static_cast<int>((g.height + nb - 1) / nb);
+    bh = (bh + ex2::BR - 1) / ex2::BR * ex2::BR;
+    return bh < 128 ? 128 : bh;
+}
+
 size_t exact_fused_carry_elems(const Geometry& g) {
-    return static_cast<size_t>(g.batch) * g.height * (g.width / ex2::SW + 1);
+    const size_t rowc = static_cast<size_t>(g.batch) * g.height * (g.width / ex2::SW + 1);
+    const int bh = exact_band_height(g);
+    const size_t colc =
+        bh > 0 ? static_cast<size_t>(g.batch) * ((g.height + bh - 1) / bh) * (g.width + 1) : 0;
+    return rowc + colc;
 }
 
 cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius, double* carries,
@@ -242,8 +265,10 @@ cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius,
     }
     ++lc.launches;
     if (e != cudaSuccess) return e;
-    ++lc.launches;
-    return kExact2[radius](in, g, carries, nsc, out, out_pitch, out_plane, s);
+    const int bh = exact_band_height(g);
+    double* ccar = carries + static_cast<size_t>(g.batch) * g.height * nsc;
+    lc.launches += bh > 0 ? 2 : 1;
+    return kExact2[radius](in, g, carries, nsc, out, out_pitch, out_plane, bh, ccar, s);
 }
 
 }  // namespace osbf_gpu

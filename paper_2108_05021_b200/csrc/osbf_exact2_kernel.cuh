@@ -340,11 +340,18 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
     }
 }
 
-template <int R, typename T>
+// CARRIES: walk the whole plane without the stencil and store the table
+// values C(cx, band*band_h - BR) of the strip's own columns for every band
+// >= 1 (ccar[(b*nbands + band)*(W+1) + cx]).  Otherwise, with band_h > 0,
+// the CTA (blockIdx.z = band) outputs rows [band*band_h, +band_h): it starts
+// one block above the band from those stored table values and walks one
+// block past it (the band's last rows need table rows up to +R).
+template <int R, typename T, bool CARRIES>
 __global__ void __launch_bounds__(NT, 2)
     exact_strip(const T* __restrict__ in, size_t pitch, size_t plane,
                 const double* __restrict__ carries, int nsc, double* __restrict__ out,
-                size_t opitch, size_t oplane, int W, int H) {
+                size_t opitch, size_t oplane, int W, int H, int band_h,
+                double* __restrict__ ccar) {
     using L = XLay<R>;
     extern __shared__ double sm[];
     double* Ubuf = sm;                          // NUB x [BR][PUB]
@@ -359,8 +366,18 @@ __global__ void __launch_bounds__(NT, 2)
     const T* src = in + static_cast<size_t>(b) * plane;
     double* outp = out + static_cast<size_t>(b) * oplane;
     const long long gbase = static_cast<long long>(b) * H;
-    const int nblocks = (H + BR - 1) / BR;
     const int tid = threadIdx.x;
+    const int nbands = band_h > 0 ? (H + band_h - 1) / band_h : 1;
+    const int band = CARRIES ? 0 : blockIdx.z;
+    int y_out_lo = 0, y_out_hi = H, y_walk0 = 0, y_walk_end = H;
+    if (!CARRIES && band_h > 0) {
+        y_out_lo = band * band_h;
+        y_out_hi = min(H, y_out_lo + band_h);
+        y_walk0 = band == 0 ? 0 : y_out_lo - BR;
+        y_walk_end = min(H, y_out_hi + BR);
+    }
+    if (CARRIES) y_walk_end = min(H, (nbands - 1) * band_h - BR);  // last band's start row
+    const int nblocks = (y_walk_end - y_walk0 + BR - 1) / BR;
     const int xe = min(X0 + TW + R - 1, W - 1);  // last R column needed
 
     double creg = 0.0;    // running table column (threads < NCC)
@@ -399,19 +416,37 @@ __global__ void __launch_bounds__(NT, 2)
         }
     };
 
-    if (tid < L::NCC) Cr[ring_row<R>(0) * L::NCC + tid] = 0.0;  // zero border row
-    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, 0, W, H, U_of(0), cs_of(0),
+    if (tid < L::NCC) {
+        const int cx = X0 - R + tid;
+        if (y_walk0 > 0 && cx >= 0 && cx <= W)
+            creg = ccar[(static_cast<size_t>(b) * nbands + band) * (W + 1) + cx];
+        unsafe = !table_value_safe(creg);
+        Cr[ring_row<R>(y_walk0) * L::NCC + tid] = creg;  // table row y_walk0 (zero border at 0)
+    }
+    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0, W, H, U_of(0), cs_of(0),
                       aligned16);
     cp_wait<0>();
     __syncthreads();
     if (nblocks > 1)  // lands during iteration 0's phase A
-        stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, BR, W, H, U_of(1), cs_of(1),
-                          aligned16);
+        stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + BR, W, H, U_of(1),
+                          cs_of(1), aligned16);
     row_prefix(0);
     __syncthreads();
     const int early = BR - R - 1 > 0 ? BR - R - 1 : 0;  // rows of block k-1 not needing block k
+    // stencil rows of block j = rows [yb, yb + BR) restricted to the band
+    auto stencil_part = [&](int j, int r_from, int r_to, int w_first, int n_w, bool safe) {
+        const int yb = y_walk0 + j * BR;
+        const int lo = max(r_from, y_out_lo - yb), hi = min(min(r_to, H - yb), y_out_hi - yb);
+        if (lo >= hi) return;
+        if (safe)
+            stencil_rows<R, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+                                  opitch);
+        else
+            stencil_rows<R, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+                                   opitch);
+    };
     for (int k = 0; k < nblocks; ++k) {
-        const int y0 = k * BR;
+        const int y0 = y_walk0 + k * BR;
         const int nrows = min(BR, H - y0);
         // Phase A: table columns of block k  ||  rows of block k-1 whose
         // windows end before block k's table rows (all but the last R+1)
@@ -429,26 +464,25 @@ __global__ void __launch_bounds__(NT, 2)
                 }
             }
             unsafe |= unsafe_here;
-        } else if (k > 0) {
-            if (safe_prev)
-                stencil_rows<R, true>(Cr, U_of(k - 1), xs, X0, y0 - BR, 0, early, L::CCW,
-                                      NT / 32 - L::CCW, W, H, outp, opitch);
-            else
-                stencil_rows<R, false>(Cr, U_of(k - 1), xs, X0, y0 - BR, 0, early, L::CCW,
-                                       NT / 32 - L::CCW, W, H, outp, opitch);
+            if (CARRIES && tid >= R && tid < L::NCC) {
+                // table row y0 + nrows is a band start row (band*band_h - BR)?
+                const int cy = y0 + nrows, cx = X0 - R + tid;
+                if ((cy + BR) % band_h == 0 && cx <= W && (tid < R + TW || cx == W)) {
+                    const int bnd = (cy + BR) / band_h;
+                    if (bnd >= 1 && bnd < nbands)
+                        ccar[(static_cast<size_t>(b) * nbands + bnd) * (W + 1) + cx] = creg;
+                }
+            }
+        } else if (!CARRIES && k > 0) {
+            stencil_part(k - 1, 0, early, L::CCW, NT / 32 - L::CCW, safe_prev);
         }
         cp_wait<0>();  // block k+1 staged
         unsafe = __syncthreads_or(unsafe);  // sticky for the strip
         // Phase B: row prefixes of block k+1  ||  the last R+1 rows of block k-1
         if (warp < L::RRW) {
             if (k + 1 < nblocks) row_prefix(k + 1);
-        } else if (k > 0) {
-            if (!unsafe)
-                stencil_rows<R, true>(Cr, U_of(k - 1), xs, X0, y0 - BR, early, BR, L::RRW,
-                                      NT / 32 - L::RRW, W, H, outp, opitch);
-            else
-                stencil_rows<R, false>(Cr, U_of(k - 1), xs, X0, y0 - BR, early, BR, L::RRW,
-                                       NT / 32 - L::RRW, W, H, outp, opitch);
+        } else if (!CARRIES && k > 0) {
+            stencil_part(k - 1, early, BR, L::RRW, NT / 32 - L::RRW, !unsafe);
         }
         __syncthreads();
         // block k+2 into the buffer S(k-1) just released; lands during k+1
@@ -456,13 +490,7 @@ __global__ void __launch_bounds__(NT, 2)
             stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + 2 * BR, W, H,
                               U_of(k + 2), cs_of(k + 2), aligned16);
     }
-    const int ylast = (nblocks - 1) * BR;
-    if (!unsafe)
-        stencil_rows<R, true>(Cr, U_of(nblocks - 1), xs, X0, ylast, 0, H - ylast, 0, NT / 32, W,
-                              H, outp, opitch);
-    else
-        stencil_rows<R, false>(Cr, U_of(nblocks - 1), xs, X0, ylast, 0, H - ylast, 0, NT / 32, W,
-                               H, outp, opitch);
+    if (!CARRIES) stencil_part(nblocks - 1, 0, BR, 0, NT / 32, !unsafe);
 }
 
 }  // namespace ex2
@@ -470,23 +498,36 @@ __global__ void __launch_bounds__(NT, 2)
 // One radius (instantiated in osbf_exact2_rNN.cu).
 template <int R>
 cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double* carries,
-                                 int nsc, double* out, size_t opitch, size_t oplane,
-                                 cudaStream_t s) {
+                                 int nsc, double* out, size_t opitch, size_t oplane, int band_h,
+                                 double* ccar, cudaStream_t s) {
     using L = ex2::XLay<R>;
-    dim3 grid((g.width + ex2::TW - 1) / ex2::TW, g.batch);
+    const int strips = (g.width + ex2::TW - 1) / ex2::TW;
+    const int nbands = band_h > 0 ? (g.height + band_h - 1) / band_h : 1;
     auto go = [&](auto tag) -> cudaError_t {
         using T = decltype(tag);
         static bool configured = false;
         if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(ex2::exact_strip<R, T>,
+            cudaError_t e = cudaFuncSetAttribute(ex2::exact_strip<R, T, false>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(L::SMEM));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(ex2::exact_strip<R, T, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(L::SMEM));
             if (e != cudaSuccess) return e;
             configured = true;
         }
-        ex2::exact_strip<R, T><<<grid, ex2::NT, L::SMEM, s>>>(
-            static_cast<const T*>(in.base), in.pitch, in.plane, carries, nsc, out, opitch, oplane,
-            g.width, g.height);
+        const T* base = static_cast<const T*>(in.base);
+        if (nbands > 1) {
+            ex2::exact_strip<R, T, true><<<dim3(strips, g.batch, 1), ex2::NT, L::SMEM, s>>>(
+                base, in.pitch, in.plane, carries, nsc, out, opitch, oplane, g.width, g.height,
+                band_h, ccar);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        ex2::exact_strip<R, T, false><<<dim3(strips, g.batch, nbands), ex2::NT, L::SMEM, s>>>(
+            base, in.pitch, in.plane, carries, nsc, out, opitch, oplane, g.width, g.height,
+            nbands > 1 ? band_h : 0, ccar);
         return cudaGetLastError();
     };
     switch (in.dtype) {

@@ -3,5 +3,6 @@
 
 namespace osbf_gpu {
 template cudaError_t exact2_launch_radius<16>(const PlaneView&, const Geometry&, double*, int,
-                                              double*, size_t, size_t, cudaStream_t);
+                                              double*, size_t, size_t, int, double*,
+                                              cudaStream_t);
 }  // namespace osbf_gpu

@@ -79,6 +79,20 @@ def test_exact_random_shapes_bit_exact(ctx, oracle_lib, seed):
     assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, r, 3)))
 
 
+@pytest.mark.parametrize("shape,r,scale", [
+    ((1, 700, 333), 1, 255.0), ((1, 1000, 97), 2, 1.0), ((1, 2049, 40), 16, 1e6),
+    ((3, 600, 200), 3, 255.0), ((1, 1537, 65), 8, 1e-300), ((2, 520, 31), 4, 1e300)])
+def test_exact_row_bands_bit_exact(ctx, oracle_lib, shape, r, scale):
+    """Tall planes with few 32-column strips run the exact strip kernel in
+    row bands that start from stored table rows; must stay bit-exact,
+    including values whose window divisions take the guarded path."""
+    rng = np.random.default_rng(sum(shape) + r)
+    p = rng.random(shape) * scale
+    got = ctx.iterate(torch_dev(p), r, 2, mode="exact").cpu().numpy()
+    want = np.stack([oracle_lib.osbf(c, r, 2, threads=8) for c in p])
+    assert np.array_equal(bits(got), bits(want))
+
+
 def test_exact_sat_bit_exact(ctx, oracle_lib):
     rng = np.random.default_rng(7)
     for h, w in [(1, 1), (3, 200), (257, 65), (300, 301)]:
