@@ -539,9 +539,28 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
     return cudaGetLastError();
 }
 
+}  // namespace fastk
+}  // namespace osbf_gpu
+
+#include "osbf_fast_stream.cuh"
+
+namespace osbf_gpu {
+namespace fastk {
+
 template <int R, bool DIAG>
 cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, size_t op,
                          size_t opl, double* means, uint8_t* sel, cudaStream_t s) {
+    if constexpr (R >= kStreamMinRadius && R <= kStreamMaxRadius && !DIAG) {
+        if (stream_enabled()) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_stream<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_stream<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_stream<R, double, false>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
     if constexpr (R <= kTmaRadius && !DIAG) {
         cudaError_t e = cudaErrorNotSupported;
         switch (in.dtype) {

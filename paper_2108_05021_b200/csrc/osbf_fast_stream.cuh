@@ -1,0 +1,272 @@
+// Fast mode, mid radii: streaming column strips with register rings.
+//
+// Included by osbf_fast_kernel.cuh (uses Band, select_store, ColFactors,
+// tma_dtype).  One CTA owns a strip of TWS = 224 output columns and a band of
+// output rows, and walks down it once:
+//
+//   * A producer warp streams the strip (plus an R-column halo each side)
+//     with TMA in chunks of CH = 2R+2 rows through a 3-4 slot ring
+//     (mbarrier full/empty pairs; hardware zero fill outside the image, so
+//     clipped windows need no special casing; the valid counts are the
+//     reference's clipped ones, integral.hpp:53-61).
+//   * Seven column warps, one thread per output column.  Per chunk each warp
+//     first forms the horizontal left arms H(x) = sum U[x-R..x] of its own
+//     32 + R columns (lanes = 16 rows x 2 odd-length segments: conflict-free,
+//     fully unrolled so every sample is loaded once) into a private slice,
+//     then walks the chunk's rows keeping vertical running sums Up/Dn of
+//     F1 = H(x), F2 = H(x+R), F3 = U(x) (the decomposition of
+//     osbf_fast_kernel.cuh) with the last 2R+2 values of each field in
+//     REGISTERS (a ring indexed by the row within the chunk, so every index
+//     is static).  Per pixel: 3 shared-memory loads for the walk, O(1) work
+//     independent of R, and each input row is read once per strip (no tile
+//     halo rows).  No CTA-wide barrier: warps only wait for their chunk.
+//
+// Running sums start at zero over a zeroed ring at the first input row (the
+// window rows above the strip's first output are the R rows of the halo), so
+// the first output already has the complete sums.  Integer inputs keep exact
+// integer sums (bit-exact first pass on uint8, as the tile kernels).
+#include <stdlib.h>
+
+#include <type_traits>
+
+namespace osbf_gpu {
+namespace fastk {
+
+constexpr int kStreamMinRadius = 5;
+constexpr int kStreamMaxRadius = 7;
+
+template <int R, typename T>
+struct SLay {
+    static constexpr int NWB = 4;               // column warps (one per SM sub-partition)
+    static constexpr int TWS = 32 * NWB;        // output columns per strip
+    static constexpr int NTS = 32 * (NWB + 1);  // + 1 TMA producer warp
+    static constexpr int L = 2 * R + 2;         // register ring length
+    static constexpr int CH = L;                // rows per chunk (ring index = row in chunk)
+    static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
+    static constexpr int RA = (R + ALIGN - 1) / ALIGN * ALIGN;  // TMA x start: X0 - RA
+    static constexpr int XOFF = RA - R;
+    static constexpr int BW0 = (TWS + RA + R + ALIGN - 1) / ALIGN * ALIGN;
+    // fp64 rows: BW = 2 mod 4 doubles, so 16 rows x 2 odd-offset segments of
+    // the arm pass hit all 16 bank pairs twice (conflict-free)
+    static constexpr int BW = sizeof(T) == 8 ? (BW0 % 4 == 2 ? BW0 : BW0 + (BW0 % 4 == 0 ? 2 : 1))
+                                             : BW0;
+    static_assert(BW <= 256, "TMA box width");
+    // per-warp arm slice: H(X0 + 32w + m), m < 32 + R, in 2 odd segments
+    static constexpr int SEGA = ((32 + R + 1) / 2) | 1;
+    static constexpr int HWP = (2 * SEGA) % 4 == 2 ? 2 * SEGA : 2 * SEGA + 2;
+    static constexpr uint32_t CHUNK_BYTES = static_cast<uint32_t>(BW) * CH * sizeof(T);
+    static constexpr size_t U_BYTES = (CHUNK_BYTES + 127) / 128 * 128;
+    static constexpr size_t U_ELEMS = U_BYTES / sizeof(T);
+    static constexpr size_t H_WARP = static_cast<size_t>(HWP) * CH;  // doubles
+    static constexpr size_t H_BYTES = NWB * H_WARP * sizeof(double);
+    static constexpr size_t PAD = 512;  // equal-length arm segments may read past the last row
+    static constexpr size_t kSmemMax = 227 * 1024;
+    // U ring depth: as deep as MINB CTAs per SM allow (3..8 slots)
+    static constexpr int MINB = R <= 5 ? 3 : 2;  // CTAs per SM (register budget)
+    static constexpr size_t kCtaSmem = (MINB == 3 ? 74 : 112) * 1024;
+    static constexpr int NU_FIT = static_cast<int>((kCtaSmem - 128 - PAD - H_BYTES) / U_BYTES);
+    static constexpr int NU = NU_FIT > 8 ? 8 : (NU_FIT < 3 ? 3 : NU_FIT);
+    static constexpr size_t SMEM = 128 + NU * U_BYTES + PAD + H_BYTES;
+    static_assert(SMEM <= kSmemMax, "stream kernel shared memory");
+};
+
+template <int R, typename T, int N>
+__device__ __forceinline__ void arm_segment(const T* __restrict__ u, double* __restrict__ h) {
+    double v[N + R];
+#pragma unroll
+    for (int i = 0; i < N + R; ++i) v[i] = to_f64(u[i]);
+    double acc = v[0];
+#pragma unroll
+    for (int i = 1; i <= R; ++i) acc += v[i];
+    h[0] = acc;
+#pragma unroll
+    for (int m = 1; m < N; ++m) {
+        acc += v[m + R] - v[m - 1];
+        h[m] = acc;
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+__global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
+    fast_stream_step(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+                     size_t out_pitch, size_t out_plane, int W, Band band, int band_rows) {
+    using Ly = SLay<R, T>;
+    constexpr int L = Ly::L, CH = Ly::CH;
+    extern __shared__ unsigned char smem_raw[];
+    // ufull: TMA landed (1 arrive + tx); uempty: slot consumed by every
+    // column warp.  Each column warp computes the arms of its own 32 + R
+    // columns (private slice, no cross-warp dependency) and then its rows;
+    // no CTA-wide barrier after the prologue.
+    __shared__ uint64_t ufull[Ly::NU], uempty[Ly::NU];
+    __shared__ double rtab[2 * R + 2];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    unsigned char* sm = smem_raw + ((128u - (base & 127u)) & 127u);
+    T* Ub = reinterpret_cast<T*>(sm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double* Hw = reinterpret_cast<double*>(sm + Ly::NU * Ly::U_BYTES + Ly::PAD) +
+                 warp * Ly::H_WARP;
+
+    const int X0 = blockIdx.x * Ly::TWS;
+    const int Y0 = band.y_out0 + blockIdx.y * band_rows;
+    const int nout = min(band_rows, band.y_end - Y0);
+    const int nchunks = (nout + 2 * R + CH - 1) / CH;
+    const int b = blockIdx.z;
+    const int ytma0 = Y0 - R - band.y_in0;  // input-buffer row of strip input row 0
+    constexpr int PRODUCER = Ly::NWB;
+
+    if (tid < 2 * R + 2) rtab[tid] = tid ? 1.0 / tid : 0.0;
+    if (tid == 0) {
+        for (int q = 0; q < Ly::NU; ++q) {
+            tma::mbar_init(&ufull[q], 1);
+            tma::mbar_init(&uempty[q], Ly::NWB);
+        }
+    }
+    __syncthreads();
+
+    if (warp == PRODUCER) {
+        if (lane == 0) {
+            for (int c = 0; c < nchunks; ++c) {
+                const int q = c % Ly::NU;
+                // slot of chunk c - NU: released once chunk c - NU + 1 is done
+                if (c >= Ly::NU) tma::mbar_wait(&uempty[q], ((c / Ly::NU) - 1) & 1);
+                tma::mbar_arrive_expect_tx(&ufull[q], Ly::CHUNK_BYTES);
+                tma::load_3d(Ub + q * Ly::U_ELEMS, &tmap, X0 - Ly::RA, ytma0 + c * CH, b,
+                             &ufull[q]);
+            }
+        }
+        return;
+    }
+
+    // Arms of this warp's slice for the chunk in U: lanes = 16 rows x 2 segments.
+    auto arms = [&](const T* U) {
+        const int rl = lane & 15, sl = lane >> 4;
+        for (int k = rl; k < CH; k += 16)
+            arm_segment<R, T, Ly::SEGA>(U + k * Ly::BW + 32 * warp + sl * Ly::SEGA + Ly::XOFF,
+                                        Hw + k * Ly::HWP + sl * Ly::SEGA);
+        __syncwarp();
+    };
+
+    // Column warps: one output column per thread.
+    const int gx = X0 + tid;
+    const int Himg = band.h_img;
+    // Rings of column PREFIX sums (slot = row within the chunk):
+    //   P1 = sum F1, P2 = sum F2, PG = sum G with G = F1 + F2 - F3 (the full
+    //   2R+1 row arm).  Each window is one difference of two prefixes:
+    //   Up = P(y) - P(y-R-1), Dn = P(y+R) - P(y-1), Full = P(y+R) - P(y-R-1).
+    double q1[L], q2[L], qg[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) q1[i] = q2[i] = qg[i] = 0.0;
+    double P1 = 0.0, P2 = 0.0, PG = 0.0;
+    const bool col_border = gx < R || gx >= W - R;
+    double* ocol = out + static_cast<size_t>(b) * out_plane + gx;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (gx < W) {  // border rows of interior columns need them too
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    // Whole chunk of interior outputs (the common case): no per-row branch,
+    // so the unrolled rows interleave.  Otherwise per-row checks.
+    // u / uprev: this column's samples in the chunk's / previous chunk's slot
+    // (the centre sample of row k sits R rows up).
+    auto chunk_rows = [&](auto interior, const double* h, const T* u, const T* uprev, int iy0,
+                          const ColFactors& cf) {
+        constexpr bool IN = decltype(interior)::value;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            const double a = h[k * Ly::HWP], c = h[k * Ly::HWP + R];
+            const double e = to_f64(u[k * Ly::BW]);
+            P1 += a;
+            P2 += c;
+            PG += (a + c) - e;
+            const int iY = (k + R + 2) % L, iYm1 = (k + R + 1) % L, iOld = (k + 1) % L;
+            const double p1y = q1[iY], p1m = q1[iYm1], p1o = q1[iOld];
+            const double p2y = q2[iY], p2m = q2[iYm1], p2o = q2[iOld];
+            const double pgy = qg[iY], pgm = qg[iYm1], pgo = qg[iOld];
+            q1[k] = P1;
+            q2[k] = P2;
+            qg[k] = PG;
+            const int iy = iy0 + k;  // output row Y0 + iy - R when iy in [R, R + nout)
+            if (IN || (iy >= R && iy < R + nout && gx < W)) {
+                const int gy = Y0 + iy - R;
+                const double uc = to_f64(k >= R ? u[(k - R) * Ly::BW] : uprev[(k - R + CH) * Ly::BW]);
+                const double S[8] = {P1 - p1m, P2 - p2m, p2y - p2o, p1y - p1o,
+                                     P1 - p1o, P2 - p2o, PG - pgm,  pgy - pgo};
+                double* o = ocol + static_cast<size_t>(gy - band.y_out0) * out_pitch;
+                if (IN || !(col_border || gy < R || gy >= Himg - R))
+                    select_store<R, EXACT_DIV, false, false>(S, uc, gx, gy, W, Himg, b, o,
+                                                             nullptr, nullptr, cf, rtab);
+                else
+                    select_store<R, EXACT_DIV, true, false>(S, uc, gx, gy, W, Himg, b, o, nullptr,
+                                                            nullptr, cf, rtab);
+            }
+        }
+    };
+    const bool warp_interior = __all_sync(0xffffffffu, gx < W && !col_border);
+    for (int c = 0; c < nchunks; ++c) {
+        const int q = c % Ly::NU, qp = (c + Ly::NU - 1) % Ly::NU;
+        tma::mbar_wait(&ufull[q], (c / Ly::NU) & 1);
+        arms(Ub + q * Ly::U_ELEMS);
+        const T* u = Ub + q * Ly::U_ELEMS + tid + Ly::RA;
+        const T* uprev = Ub + qp * Ly::U_ELEMS + tid + Ly::RA;
+        const double* h = Hw + lane;
+        const int iy0 = c * CH - R;  // strip row index (input coords) of the k = 0 output
+        const int gy0 = Y0 + iy0 - R;
+        if (warp_interior && iy0 >= R && iy0 + L <= R + nout && gy0 >= R && gy0 + L <= Himg - R)
+            chunk_rows(std::true_type{}, h, u, uprev, iy0, cf);
+        else
+            chunk_rows(std::false_type{}, h, u, uprev, iy0, cf);
+        __syncwarp();  // slice and slot reads done before reuse
+        // the previous chunk's slot (centre samples) is free now
+        if (lane == 0 && c > 0) tma::mbar_arrive(&uempty[qp]);
+    }
+}
+
+inline bool stream_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("OSBF_GPU_STREAM");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// Returns cudaErrorNotSupported (no launch) when the layout is not TMA-able.
+template <int R, typename T, bool EXACT_DIV>
+cudaError_t launch_stream(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                          size_t opl, cudaStream_t s) {
+    using Ly = SLay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::CH))
+        return cudaErrorNotSupported;
+    static bool configured = false;
+    static int sms = 148;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fast_stream_step<R, T, EXACT_DIV>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Ly::SMEM));
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        configured = true;
+    }
+    // Row bands only when strips x planes leave SMs idle (each band re-reads
+    // a 2R-row halo).
+    const int strips = (g.width + Ly::TWS - 1) / Ly::TWS;
+    const long long ctas = static_cast<long long>(strips) * g.batch;
+    int band_rows = g.height;
+    if (ctas < 2LL * sms) {
+        const long long nb = (2LL * sms + ctas - 1) / ctas;
+        band_rows = static_cast<int>((g.height + nb - 1) / nb);
+        band_rows = max(band_rows, 8 * Ly::CH);
+    }
+    dim3 grid(strips, (g.height + band_rows - 1) / band_rows, g.batch);
+    fast_stream_step<R, T, EXACT_DIV><<<grid, Ly::NTS, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                                      band_of(g), band_rows);
+    return cudaGetLastError();
+}
+
+}  // namespace fastk
+}  // namespace osbf_gpu

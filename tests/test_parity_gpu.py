@@ -205,11 +205,17 @@ def test_in_place_and_pitched(ctx, oracle_lib):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
 
 
-@pytest.mark.parametrize("r", [2, 7])
+STREAM_RADII = range(5, 8)  # fast radii served by the streaming column-strip kernel
+
+
+@pytest.mark.parametrize("r", [2, 7, 12])
 def test_row_bands_equal_whole_image(ctx, r):
     """osbf_gpu_step_band over 64-aligned row bands (halos copied from the
     previous pass, as the multi-GPU exchange does) is bit-identical to the
-    whole-image fast pass; unaligned bands stay within the float tolerance."""
+    whole-image fast pass for the tile kernels; the streaming kernel's running
+    sums start at each band's first row, so there the bands agree to fp64
+    rounding (1e-9 of the range).  Unaligned bands stay within the float
+    tolerance."""
     import torch
 
     from paper_2108_05021_b200.dist import BandLayout
@@ -226,7 +232,10 @@ def test_row_bands_equal_whole_image(ctx, r):
                 src = cur[lay.buf_row0:lay.buf_row0 + lay.buf_rows].contiguous()
                 ctx.step_band(src, lay.buf_row0, nxt[lay.row0:lay.row1], lay.row0, lay.rows, h, r)
             cur = nxt
-        assert torch.equal(cur.view(torch.int64), want.view(torch.int64)), world
+        if r in STREAM_RADII:
+            assert float((cur - want).abs().max()) <= 1e-9, world
+        else:
+            assert torch.equal(cur.view(torch.int64), want.view(torch.int64)), world
     # unaligned bands (tile grid shifted): same result within tolerance
     cur = x.clone()
     cuts = [0, 250, 333, 700]
