@@ -79,6 +79,7 @@ struct osbf_ctx {
     DevBuf host_in, host_out;  // staging for the host entry points
     osbf_gpu::LaunchCounter lc;
     int passes_per_launch = 1;  // fast mode temporal blocking: 1 or 2
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host entry points: copy overlap
 };
 
 namespace {
@@ -239,6 +240,8 @@ osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx) {
     ctx->sat.release();
     ctx->host_in.release();
     ctx->host_out.release();
+    if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+    if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return OSBF_OK;
@@ -446,17 +449,74 @@ osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h
     OSBF_CUDA(ctx->host_in.ensure(n * dtype_size(in_dtype)), "alloc input");
     OSBF_CUDA(ctx->host_out.ensure(n * sizeof(double)), "alloc output");
     cudaStream_t s = ctx->stream;
-    OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * dtype_size(in_dtype),
-                              cudaMemcpyHostToDevice, s),
-              "H2D");
     const size_t plane = static_cast<size_t>(width) * height;
-    st = osbf_gpu_iterate(ctx, in_dtype, ctx->host_in.ptr, width, plane, ctx->host_out.as<double>(),
-                          width, plane, width, height, batch, radius, iterations, mode, s);
+    const size_t in_bytes = plane * dtype_size(in_dtype);
+    const char* hin = static_cast<const char*>(h_in);
+    char* din = static_cast<char*>(ctx->host_in.ptr);
+    double* dout = ctx->host_out.as<double>();
+    // Planes are independent: large batches go through in chunks so the
+    // upload of chunk j+1 and the download of chunk j-1 (two copy streams)
+    // overlap the passes of chunk j (compute stream).  Results do not depend
+    // on the chunking.
+    const int chunks = (batch >= 4 && n * sizeof(double) >= (64u << 20)) ? (batch < 8 ? batch : 8)
+                                                                           : 1;
+    if (chunks == 1) {
+        OSBF_CUDA(cudaMemcpyAsync(din, hin, n * dtype_size(in_dtype), cudaMemcpyHostToDevice, s),
+                  "H2D");
+        st = osbf_gpu_iterate(ctx, in_dtype, din, width, plane, dout, width, plane, width, height,
+                              batch, radius, iterations, mode, s);
+        if (st != OSBF_OK) return st;
+        OSBF_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, s),
+                  "D2H");
+        OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+        return OSBF_OK;
+    }
+    if (!ctx->copy_in)
+        OSBF_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "stream");
+    if (!ctx->copy_out)
+        OSBF_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "stream");
+    cudaEvent_t ev[2 * 8];
+    int nev = 0;
+    for (; nev < 2 * chunks; ++nev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ev[nev], cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+            return cuda_fail(e, "cudaEventCreate");
+        }
+    }
+    auto cleanup = [&] {
+        for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+    };
+    for (int j = 0; j < chunks && st == OSBF_OK; ++j) {
+        const int b0 = static_cast<int>(static_cast<long long>(batch) * j / chunks);
+        const int b1 = static_cast<int>(static_cast<long long>(batch) * (j + 1) / chunks);
+        const size_t nb = static_cast<size_t>(b1 - b0);
+        cudaError_t e = cudaMemcpyAsync(din + b0 * in_bytes, hin + b0 * in_bytes, nb * in_bytes,
+                                        cudaMemcpyHostToDevice, ctx->copy_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * j], ctx->copy_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * j], 0);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "H2D");
+            break;
+        }
+        st = osbf_gpu_iterate(ctx, in_dtype, din + b0 * in_bytes, width, plane, dout + b0 * plane,
+                              width, plane, width, height, b1 - b0, radius, iterations, mode, s);
+        if (st != OSBF_OK) break;
+        e = cudaEventRecord(ev[2 * j + 1], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_out, ev[2 * j + 1], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out + b0 * plane, dout + b0 * plane, nb * plane * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctx->copy_out);
+        if (e != cudaSuccess) st = cuda_fail(e, "D2H");
+    }
+    cudaError_t e1 = cudaStreamSynchronize(ctx->copy_out);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaError_t e3 = cudaStreamSynchronize(ctx->copy_in);
+    cleanup();
     if (st != OSBF_OK) return st;
-    OSBF_CUDA(cudaMemcpyAsync(h_out, ctx->host_out.ptr, n * sizeof(double), cudaMemcpyDeviceToHost,
-                              s),
-              "D2H");
-    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    if (e1 != cudaSuccess) return cuda_fail(e1, "sync");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "sync");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
     return OSBF_OK;
 }
 

@@ -241,27 +241,19 @@ cudaError_t launch_stream(const PlaneView& in, const Geometry& g, double* out, s
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::CH))
         return cudaErrorNotSupported;
     static bool configured = false;
-    static int sms = 148;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(fast_stream_step<R, T, EXACT_DIV>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(Ly::SMEM));
         if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         configured = true;
     }
-    // Row bands only when strips x planes leave SMs idle (each band re-reads
-    // a 2R-row halo).
+    // Tall images walk in 512-row bands (each band re-reads a 2R-row halo) so
+    // a single plane still fills the SMs.  The split depends on the image
+    // height only, never on the batch size, so results do not depend on how
+    // a batch is chunked.
     const int strips = (g.width + Ly::TWS - 1) / Ly::TWS;
-    const long long ctas = static_cast<long long>(strips) * g.batch;
-    int band_rows = g.height;
-    if (ctas < 2LL * sms) {
-        const long long nb = (2LL * sms + ctas - 1) / ctas;
-        band_rows = static_cast<int>((g.height + nb - 1) / nb);
-        band_rows = max(band_rows, 8 * Ly::CH);
-    }
+    const int band_rows = g.height <= 1024 ? g.height : 512;
     dim3 grid(strips, (g.height + band_rows - 1) / band_rows, g.batch);
     fast_stream_step<R, T, EXACT_DIV><<<grid, Ly::NTS, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                       band_of(g), band_rows);

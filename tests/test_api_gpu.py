@@ -70,3 +70,17 @@ def test_dtype_promotion_is_exact(ctx, oracle_lib):
     for a in (u8, f32):
         got = ctx.iterate(torch.from_numpy(a).cuda(), 2, 2, mode="exact").cpu().numpy()
         assert np.array_equal(bits(got), bits(oracle_lib.osbf(a.astype(np.float64), 2, 2)))
+
+
+@pytest.mark.parametrize("mode,r", [("fast", 2), ("fast", 6), ("exact", 3)])
+def test_host_batch_pipeline_matches_device_path(ctx, mode, r):
+    """Host-buffer batches >= 64 MB go through in overlapped chunks (upload /
+    passes / download on three streams); the result is bit-identical to one
+    device-resident launch over the whole batch."""
+    import torch
+
+    rng = np.random.default_rng(r)
+    x = (rng.random((9, 1024, 1024)) * 255).astype(np.float32)  # 72 MB of fp64 output
+    got = ctx.osbf_host(x, r, 2, mode=mode)
+    want = ctx.iterate(torch.from_numpy(x).cuda(), r, 2, mode=mode).cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
