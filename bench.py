@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--radius", type=int, default=None)
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=("push", "nccl"), default="push",
+                    help="C5 halo exchange: fused into the pass kernel (symmetric memory) "
+                         "or NCCL send/recv after it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -275,7 +278,8 @@ def run_reference(args, world, rank):
 
 def run_c5(args, world, rank, local):
     """C5: one 32768^2 float32 image, row bands across ranks (strong scaling),
-    fast mode, per-pass halo exchange (NCCL send/recv) between neighbours."""
+    fast mode, per-pass halo exchange between neighbours (fused into the pass
+    kernel through symmetric memory, or NCCL send/recv with --exchange nccl)."""
     import torch
 
     from paper_2108_05021_b200 import synth
@@ -289,7 +293,7 @@ def run_c5(args, world, rank, local):
     x = synth.make_c5_on_device(H, W, seed=5)  # identical on every rank (Philox)
     lay = BandLayout.make(H, W, r, world, rank)
     band = x[lay.row0:lay.row1]
-    runner = RowBandOSBF(lay, rank, world)
+    runner = RowBandOSBF(lay, rank, world, exchange=args.exchange)
     for _ in range(max(args.warmup, 0)):
         runner.run(band, iters)
     torch.cuda.synchronize()
@@ -323,7 +327,10 @@ def run_c5(args, world, rank, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(cfg, r, iters), "height": H, "width": W,
                    "radius": r, "iterations": iters, "mode": "fast",
-                   "parallelism": f"row bands x{world}, {r}-row halo exchange per pass (NCCL)",
+                   "parallelism": f"row bands x{world}, {r}-row halo exchange per pass "
+                                  + ("(fused: pass kernel stores into the neighbours' "
+                                     "symmetric-memory halos + device barrier)"
+                                     if args.exchange == "push" else "(NCCL send/recv)"),
                    "l2": "inputs (8.6 GB fp64 per buffer) larger than L2"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),

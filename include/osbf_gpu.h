@@ -143,6 +143,24 @@ osbf_status osbf_gpu_step_band(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
                                size_t out_pitch, int out_row0, int out_rows, int width,
                                int image_height, int radius, osbf_mode mode, void* stream);
 
+/*
+ * osbf_gpu_step_band with the halo exchange fused into the pass: output rows
+ * [out_row0, out_row0 + push_rows) are also stored to d_push_up (the upper
+ * neighbour's bottom halo rows, row pitch push_pitch elements) and rows
+ * [out_row0 + out_rows - push_rows, out_row0 + out_rows) to d_push_down (the
+ * lower neighbour's top halo rows).  The push pointers may be peer memory
+ * (NVLink / symmetric memory) or NULL (no neighbour on that side); the
+ * caller orders the next pass after every rank's push (e.g. a device-side
+ * barrier).  Replaces the separate send/recv step the reference does not
+ * have (it is single-node CPU).
+ */
+osbf_status osbf_gpu_step_band_push(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                                    size_t in_pitch, int in_row0, int in_rows, double* d_out,
+                                    size_t out_pitch, int out_row0, int out_rows, int width,
+                                    int image_height, int radius, osbf_mode mode,
+                                    double* d_push_up, double* d_push_down, int push_rows,
+                                    size_t push_pitch, void* stream);
+
 /* ---- host-buffer entry points (what the drop-in C++ API calls) ------------ */
 
 /* osbf::osbf on host memory: copies in, filters, copies out, synchronizes.

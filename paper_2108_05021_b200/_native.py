@@ -50,6 +50,9 @@ SIGNATURES = [
     ("osbf_gpu_step_band", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_int, _c_int, _c_void_p, _c_size, _c_int, _c_int,
       _c_int, _c_int, _c_int, _c_int, _c_void_p]),
+    ("osbf_gpu_step_band_push", _c_int,
+     [_c_void_p, _c_int, _c_void_p, _c_size, _c_int, _c_int, _c_void_p, _c_size, _c_int, _c_int,
+      _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_int, _c_size, _c_void_p]),
     ("osbf_gpu_osbf_host", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int]),
     ("osbf_gpu_osbf_step_host", _c_int,

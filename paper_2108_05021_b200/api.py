@@ -231,11 +231,15 @@ class Context:
         return c.view(*src.shape[:-2], h + 1, w + 1)
 
     def step_band(self, src, in_row0: int, out, out_row0: int, out_rows: int,
-                  image_height: int, radius: int, mode="fast", stream=None):
+                  image_height: int, radius: int, mode="fast", stream=None,
+                  push_up=None, push_down=None, push_rows: int = 0):
         """One fast pass over a row band (osbf_gpu_step_band).  ``src``: CUDA
         tensor (in_rows, W) holding global rows [in_row0, in_row0+in_rows);
         ``out``: fp64 CUDA tensor whose rows receive global rows
-        [out_row0, out_row0 + out_rows)."""
+        [out_row0, out_row0 + out_rows).  ``push_up`` / ``push_down``: fp64
+        (push_rows, W) views of the neighbours' halo rows (local or peer
+        memory) that the pass also writes its first / last ``push_rows`` rows
+        into (osbf_gpu_step_band_push: the halo exchange fused into the pass)."""
         import torch
 
         if src.dim() != 2 or out.dim() != 2 or src.stride(1) != 1 or out.stride(1) != 1:
@@ -244,10 +248,23 @@ class Context:
             raise InvalidArgument("band output must be float64")
         if stream is None:
             stream = torch.cuda.current_stream(src.device).cuda_stream
-        _check(self._lib.osbf_gpu_step_band(
+        pitch = 0
+        for t in (push_up, push_down):
+            if t is not None:
+                if t.dtype != torch.float64 or t.dim() != 2 or t.stride(1) != 1:
+                    raise InvalidArgument("push targets must be 2-D row-major float64")
+                if t.shape[0] < push_rows or t.shape[1] < src.shape[1]:
+                    raise InvalidArgument("push target smaller than push_rows x width")
+                if pitch and t.stride(0) != pitch:
+                    raise InvalidArgument("push targets must share one row pitch")
+                pitch = t.stride(0)
+        _check(self._lib.osbf_gpu_step_band_push(
             self.handle, _dtype_code(src), ctypes.c_void_p(src.data_ptr()), src.stride(0), in_row0,
             src.shape[0], ctypes.c_void_p(out.data_ptr()), out.stride(0), out_row0, out_rows,
-            src.shape[1], image_height, radius, _mode_code(mode), ctypes.c_void_p(stream)))
+            src.shape[1], image_height, radius, _mode_code(mode),
+            ctypes.c_void_p(push_up.data_ptr() if push_up is not None else 0),
+            ctypes.c_void_p(push_down.data_ptr() if push_down is not None else 0),
+            push_rows if pitch else 0, pitch, ctypes.c_void_p(stream)))
         return out
 
     # -- host arrays (the drop-in path: H2D, filter, D2H inside the call) ----

@@ -394,7 +394,22 @@ osbf_status osbf_gpu_step_band(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
                                size_t in_pitch, int in_row0, int in_rows, double* d_out,
                                size_t out_pitch, int out_row0, int out_rows, int width,
                                int image_height, int radius, osbf_mode mode, void* stream) {
+    return osbf_gpu_step_band_push(ctx, in_dtype, d_in, in_pitch, in_row0, in_rows, d_out,
+                                   out_pitch, out_row0, out_rows, width, image_height, radius,
+                                   mode, nullptr, nullptr, 0, 0, stream);
+}
+
+osbf_status osbf_gpu_step_band_push(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                                    size_t in_pitch, int in_row0, int in_rows, double* d_out,
+                                    size_t out_pitch, int out_row0, int out_rows, int width,
+                                    int image_height, int radius, osbf_mode mode,
+                                    double* d_push_up, double* d_push_down, int push_rows,
+                                    size_t push_pitch, void* stream) {
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (push_rows < 0 || push_rows > out_rows)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "push_rows %d outside [0, out_rows]", push_rows);
+    if (push_rows > 0 && (d_push_up || d_push_down) && push_pitch < static_cast<size_t>(width))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "push pitch smaller than width");
     osbf_status st;
     if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
     if ((st = check_mode(mode)) != OSBF_OK) return st;
@@ -426,6 +441,12 @@ osbf_status osbf_gpu_step_band(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
     g.in_row0 = in_row0;
     g.out_row0 = out_row0;
     g.in_rows = in_rows;
+    if (push_rows > 0) {
+        g.push_up = d_push_up;
+        g.push_dn = d_push_down;
+        g.push_rows = push_rows;
+        g.push_pitch = push_pitch;
+    }
     const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_pitch * in_rows};
     OSBF_CUDA(osbf_gpu::fast_step(input, g, radius, d_out, out_pitch, out_pitch * out_rows, nullptr,
                                   nullptr, pick_stream(ctx, stream), ctx->lc),

@@ -52,9 +52,36 @@ struct Band {
     int y_in0;   // global row of input buffer row 0
     int y_out0;  // global row of output buffer row 0 (first output row)
     int y_end;   // one past the last output row (global)
+    double* push_up;  // fused halo push (see Geometry); null = none
+    double* push_dn;
+    int push_rows;
+    long long push_pitch;
 };
 inline Band band_of(const Geometry& g) {
-    return Band{g.img_h(), g.in_row0, g.out_row0, g.out_row0 + g.height};
+    return Band{g.img_h(),  g.in_row0,  g.out_row0,    g.out_row0 + g.height,
+                g.push_up,  g.push_dn,  g.push_rows,   static_cast<long long>(g.push_pitch)};
+}
+
+// Fused halo exchange: a band's first / last push_rows output rows are also
+// written straight into the neighbours' halo rows (peer memory over NVLink
+// when the ranks are GPUs), so no separate exchange step follows the pass.
+// Each thread forwards the rows [ya, yb) of column gx it has just stored to
+// outp (row gy at (gy - y_out0) * pitch + gx): a re-read of its own stores,
+// outside the per-pixel loop.
+__device__ __forceinline__ void push_tail(const Band& bd, const double* outp, size_t pitch, int gx,
+                                          int ya, int yb) {
+    if (bd.push_rows == 0) return;
+    if (bd.push_up) {
+        for (int gy = max(ya, bd.y_out0); gy < min(yb, bd.y_out0 + bd.push_rows); ++gy)
+            bd.push_up[static_cast<long long>(gy - bd.y_out0) * bd.push_pitch + gx] =
+                outp[static_cast<size_t>(gy - bd.y_out0) * pitch + gx];
+    }
+    if (bd.push_dn) {
+        const int y0 = bd.y_end - bd.push_rows;
+        for (int gy = max(ya, y0); gy < min(yb, bd.y_end); ++gy)
+            bd.push_dn[static_cast<long long>(gy - y0) * bd.push_pitch + gx] =
+                outp[static_cast<size_t>(gy - bd.y_out0) * pitch + gx];
+    }
 }
 
 template <int R>
@@ -176,13 +203,18 @@ struct ColFactors {
 // Means, |a-u| selection and the store for one pixel (S = the eight window
 // sums in reference order, u = the centre sample).
 template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
-__device__ __forceinline__ void select_store(const double (&S)[8], double u, int gx, int gy,
+__device__ __forceinline__ double select_store(const double (&S)[8], double u, int gx, int gy,
                                              int W, int H, int b, double* __restrict__ o,
                                              double* __restrict__ means,
                                              uint8_t* __restrict__ sel, const ColFactors& cf,
                                              const double* __restrict__ rtab) {
-    constexpr double kRq = 1.0 / ((R + 1) * (R + 1));
-    constexpr double kRh = 1.0 / ((R + 1) * (2 * R + 1));
+    // Interior reciprocals formed exactly as the border path forms them
+    // (product of the per-axis reciprocals), so a pixel gets the same factor
+    // whichever tile kind it sits in: results do not depend on the tiling and
+    // row bands equal the whole image bit for bit.
+    constexpr double kR1 = 1.0 / (R + 1), kR2 = 1.0 / (2 * R + 1);
+    constexpr double kRq = kR1 * kR1;
+    constexpr double kRh = kR1 * kR2;
     constexpr int kNq = (R + 1) * (R + 1), kNh = (R + 1) * (2 * R + 1);
     if (EXACT_DIV || DIAG) {
         // Reference arithmetic: a_i = S_i / n_i (IEEE), d_i = |a_i - u|,
@@ -211,7 +243,7 @@ __device__ __forceinline__ void select_store(const double (&S)[8], double u, int
         }
         if (DIAG && sel) sel[pix] = static_cast<uint8_t>(best_id);
         if (!DIAG || o) *o = best;
-        return;
+        return best;
     }
     // 1/n_i: interior constants, or products of clipped row/column factors
     // 1/n_row * 1/n_col from the per-CTA table (border tiles).
@@ -234,7 +266,9 @@ __device__ __forceinline__ void select_store(const double (&S)[8], double u, int
     auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
     const double best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
                              pick(pick(d[4], d[5]), pick(d[6], d[7])));
-    *o = u + best;
+    const double v = u + best;
+    *o = v;
+    return v;
 }
 
 // Phase B for one thread: output column x, rows [y0, y0 + SEGB) of the tile.
@@ -372,6 +406,10 @@ __global__ void __launch_bounds__(NT, Lay<R>::template min_ctas<EXACT_DIV || DIA
         column_walk<R, EXACT_DIV, true, DIAG>(Us, Hs, X0, Y0, W, band, b, outp, out_pitch,
                                               means, sel, rtab);
     }
+    if (!DIAG && band.push_rows && outp) {  // row-band mode with the fused halo push
+        const int gx = X0 + threadIdx.x % TW, ya = Y0 + (threadIdx.x / TW) * SEGB;
+        if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + SEGB, band.y_end));
+    }
 }
 
 template <int R, typename T, bool EXACT_DIV, bool DIAG>
@@ -506,6 +544,10 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3
         direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
     else
         direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
+    if (band.push_rows) {  // row-band mode with the fused halo push
+        const int gx = X0 + threadIdx.x % TW, ya = Y0 + (threadIdx.x / TW) * Ly::SEGT;
+        if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
+    }
 }
 
 template <typename T>

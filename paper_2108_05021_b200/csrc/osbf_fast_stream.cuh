@@ -219,6 +219,8 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
         // the previous chunk's slot (centre samples) is free now
         if (lane == 0 && c > 0) tma::mbar_arrive(&uempty[qp]);
     }
+    if (gx < W)
+        push_tail(band, out + static_cast<size_t>(b) * out_plane, out_pitch, gx, Y0, Y0 + nout);
 }
 
 inline bool stream_enabled() {

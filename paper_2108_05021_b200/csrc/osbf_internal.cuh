@@ -30,6 +30,15 @@ struct Geometry {
     int in_row0 = 0;
     int out_row0 = 0;
     int in_rows = -1;
+    // Fused halo push (row bands, fast mode): output rows [out_row0,
+    // out_row0 + push_rows) are also stored to push_up (the upper
+    // neighbour's bottom halo rows, pitch push_pitch) and rows
+    // [out_row0 + height - push_rows, out_row0 + height) to push_dn (the
+    // lower neighbour's top halo).  The pointers may be peer (NVLink) memory.
+    double* push_up = nullptr;
+    double* push_dn = nullptr;
+    int push_rows = 0;
+    size_t push_pitch = 0;
     int img_h() const { return img_height < 0 ? height : img_height; }
     int in_h() const { return in_rows < 0 ? height : in_rows; }
 };

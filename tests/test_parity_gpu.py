@@ -248,6 +248,50 @@ def test_row_bands_equal_whole_image(ctx, r):
     assert float((cur - want).abs().max()) <= FLOAT_TOL
 
 
+@pytest.mark.parametrize("r", [2, 4, 6])
+def test_row_bands_fused_push_equal_whole_image(ctx, r):
+    """The fused exchange (osbf_gpu_step_band_push via dist.RowBandOSBF
+    exchange='push'): every band's pass also stores its boundary rows into
+    the neighbours' halo rows.  Emulated here as three ranks on one device
+    (their "symmetric" buffers are local allocations, passes run one after
+    another on one stream, so no kernel waits on another); the result equals
+    the whole-image pass (bit-identical for the tile kernels, fp64 rounding
+    for the streaming r=5..7 kernel)."""
+    import torch
+
+    from paper_2108_05021_b200.dist import BandLayout, RowBandOSBF
+
+    h, w, iters, world = 700, 300, 3, 3
+    x = torch.from_numpy(np.random.default_rng(10 + r).random((h, w))).cuda()
+    want = ctx.iterate(x, r, iters, mode="fast")
+    lays = [BandLayout.make(h, w, r, world, q) for q in range(world)]
+    slot = max(q.buf_rows for q in lays) * w
+    flats = [torch.full((2 * slot,), float("nan"), dtype=torch.float64, device="cuda")
+             for _ in range(world)]
+    ranks = [RowBandOSBF(lays[q], q, world, exchange="push", peer_buffers=lambda q: flats[q],
+                         sync=lambda: None) for q in range(world)]
+    for q, rb in enumerate(ranks):
+        rb.prime(x[lays[q].row0:lays[q].row1])
+        buf = rb._bufs[0]  # initial halos straight from the image (the emulated exchange)
+        buf[:lays[q].halo_top] = x[lays[q].row0 - lays[q].halo_top:lays[q].row0]
+        top = lays[q].halo_top + lays[q].rows
+        buf[top:] = x[lays[q].row1:lays[q].row1 + lays[q].halo_bot]
+    for it in range(iters):
+        for rb in ranks:
+            rb.one_pass(last=it + 1 == iters)
+    got = torch.cat([rb.result() for rb in ranks])
+    if r in STREAM_RADII:
+        assert float((got - want).abs().max()) <= 1e-9
+    else:
+        assert torch.equal(got.view(torch.int64), want.view(torch.int64))
+    # the pushed halos hold the neighbours' final rows
+    for q in range(world - 1):
+        lo, hi = ranks[q], ranks[q + 1]
+        top = lays[q].halo_top + lays[q].rows
+        assert torch.equal(lo._bufs[lo._cur][top:], hi.result()[:r])
+        assert torch.equal(hi._bufs[hi._cur][:r], lo.result()[-r:])
+
+
 def test_row_band_errors(ctx):
     import torch
 
