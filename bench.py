@@ -338,6 +338,8 @@ def run_c5(args, world, rank, local):
                      "avg_pass_ms_incl_exchange": round(kernel_ms, 4)},
         "gpu_launches": launches,
         "clocks": clk,
+        "exchange": runner.exchange if world > 1 else "none (1 rank)",
+        **({"exchange_note": runner.exchange_note} if runner.exchange_note else {}),
         "e2e": None,
         "e2e_note": "C5 keeps the 4 GiB image device-resident; e2e is reported on C4",
     }

@@ -137,6 +137,7 @@ class RowBandOSBF:
         self._peer_buffers = peer_buffers
         self._sync = sync
         self._bufs = None
+        self.exchange_note = None
 
     def _gpu_step(self, src, lay: BandLayout, dst_band, push=None) -> None:
         if self._ctx is None:
@@ -170,10 +171,19 @@ class RowBandOSBF:
         self._slot = max(q.buf_rows for q in self._layouts()) * lay.width
         if self._peer_buffers is None:
             import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm_mem
 
-            flat = symm_mem.empty(2 * self._slot, dtype=torch.float64, device=device)
-            hdl = symm_mem.rendezvous(flat, self.group or dist.group.WORLD)
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+
+                flat = symm_mem.empty(2 * self._slot, dtype=torch.float64, device=device)
+                hdl = symm_mem.rendezvous(flat, self.group or dist.group.WORLD)
+            except Exception as e:  # no peer-mappable memory on this system
+                # the exchange mechanism (not the filter) falls back to NCCL
+                # send/recv, recorded in exchange_note; every rank takes the
+                # same branch because rendezvous is collective
+                self.exchange = "nccl"
+                self.exchange_note = f"symmetric memory unavailable ({type(e).__name__}: {e})"
+                return self.buffers(device)
             self._hdl = hdl
             self._flat = flat
             self._peer_buffers = lambda q: hdl.get_buffer(q, (2 * self._slot,), torch.float64)
