@@ -121,6 +121,20 @@ osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const v
                                      uint8_t* d_sel, osbf_mode mode, void* stream);
 
 /*
+ * Paper Algorithm 3 — the reference's fast_osbf (filters2d.hpp:105-154) —
+ * bit-identical: per iteration the whole-image SAT in the reference's order,
+ * the quarter field Q(x,y) = rect_mean(x-r, y-r, x, y), then the 8
+ * candidates from the clamped shifted quarters and their pairwise averages,
+ * strict-< first minimum of |c - u|.  Same buffer conventions as
+ * osbf_gpu_iterate.  radius < 1 is INVALID_ARGUMENT even for 0 iterations
+ * (filters2d.hpp:107-110).
+ */
+osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                              size_t in_pitch, size_t in_plane_stride, double* d_out,
+                              size_t out_pitch, size_t out_plane_stride, int width, int height,
+                              int batch, int radius, int iterations, void* stream);
+
+/*
  * Whole-image summed-area table, bit-identical to SummedAreaTable
  * (integral.hpp:16-30): d_cumsum is fp64 [batch][height+1][width+1].
  */
@@ -180,6 +194,18 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
                                               double* const* h_out, int channels, int width,
                                               int height, int radius, int iterations,
                                               osbf_mode mode);
+
+/* osbf::fast_osbf on host memory (batch planes back to back), like
+ * osbf_gpu_osbf_host. */
+osbf_status osbf_gpu_fast_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                                    double* h_out, int width, int height, int batch, int radius,
+                                    int iterations);
+
+/* osbf::filter_multichannel with FilterVariant::OsbfFast (filters2d.hpp:386):
+ * fast_osbf on every channel (one batched launch per pass). */
+osbf_status osbf_gpu_filter_multichannel_fast_host(osbf_ctx* ctx, const double* const* h_in,
+                                                   double* const* h_out, int channels, int width,
+                                                   int height, int radius, int iterations);
 
 /* SummedAreaTable construction (integral.hpp:16-30) for host planes. */
 osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,

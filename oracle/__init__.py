@@ -65,6 +65,7 @@ class Oracle:
         lib.oracle_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
         lib.oracle_subwindow_means.argtypes = [_dp] + [ctypes.c_int] * 5 + [_dp]
         lib.oracle_sub_windows.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        lib.oracle_fast_osbf.argtypes = lib.oracle_osbf.argtypes
         self.lib = lib
 
     def sub_windows(self, r: int):
@@ -81,6 +82,16 @@ class Oracle:
         st = self.lib.oracle_osbf_mt(_ptr(p), _ptr(out), w, h, r, iterations, threads)
         if st:
             raise CheckerError(st, "osbf")
+        return out
+
+    def fast_osbf(self, plane, r: int, iterations: int) -> np.ndarray:
+        """filters2d.hpp:105-154 (paper Algorithm 3)."""
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.oracle_fast_osbf(_ptr(p), _ptr(out), w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "fast_osbf")
         return out
 
     def osbf_step(self, plane, r: int, with_selection: bool = False):
@@ -125,6 +136,9 @@ class Reference:
         lib.ref_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.ref_osbf_step.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.ref_filter_multichannel.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
+        lib.ref_filter_multichannel_fast.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
+        lib.ref_fast_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int]
         lib.ref_sat.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_subwindow_means.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _u8p]
         lib.ref_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
@@ -164,13 +178,25 @@ class Reference:
             raise CheckerError(st, "ref osbf_step")
         return out
 
-    def filter_multichannel(self, planes, r: int, iterations: int) -> np.ndarray:
+    def filter_multichannel(self, planes, r: int, iterations: int,
+                            variant: str = "exact") -> np.ndarray:
         p = _as_f64(planes)
         c, h, w = p.shape
         out = np.empty_like(p)
-        st = self.lib.ref_filter_multichannel(_ptr(p), _ptr(out), c, w, h, r, iterations)
+        fn = (self.lib.ref_filter_multichannel if variant == "exact"
+              else self.lib.ref_filter_multichannel_fast)
+        st = fn(_ptr(p), _ptr(out), c, w, h, r, iterations)
         if st:
             raise CheckerError(st, "ref filter_multichannel")
+        return out
+
+    def fast_osbf(self, plane, r: int, iterations: int) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.ref_fast_osbf(_ptr(p), _ptr(out), w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "ref fast_osbf")
         return out
 
     def sat(self, plane) -> np.ndarray:

@@ -200,3 +200,55 @@ int oracle_osbf_mt(const double* in, double* out, int w, int h, int r, int itera
                    int threads) {
     return osbf_impl(in, out, w, h, r, iterations, threads);
 }
+
+/* filters2d.hpp:105-154.  Same operation order as the reference: the
+ * quarter mean is rect_mean (integral.hpp:64-69: ((A-B)-C)+D, then one IEEE
+ * division by the clipped count); the half candidates are 0.5 * (a + b) in
+ * the listed order; selection is the strict-< first minimum of |c - u|. */
+int oracle_fast_osbf(const double* in, double* out, int w, int h, int r, int iterations) {
+    if (r < 1) return ORACLE_ERR_INVALID_ARGUMENT;          /* :107-108 */
+    if (iterations < 0) return ORACLE_ERR_INVALID_ARGUMENT; /* :109-110 */
+    if (w < 1 || h < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h;
+    double* cur = (double*)malloc(sizeof(double) * n);
+    double* nxt = (double*)malloc(sizeof(double) * n);
+    double* q = (double*)malloc(sizeof(double) * n);
+    double* c = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1));
+    if (!cur || !nxt || !q || !c) {
+        free(cur); free(nxt); free(q); free(c);
+        return ORACLE_ERR_INVALID_ARGUMENT;
+    }
+    memcpy(cur, in, sizeof(double) * n);
+    for (int it = 0; it < iterations; ++it) {
+        oracle_sat_build(cur, w, h, c);
+        for (int y = 0; y < h; ++y)          /* :116-119 */
+            for (int x = 0; x < w; ++x)
+                oracle_rect_mean(c, w, h, x - r, y - r, x, y, &q[(size_t)y * w + x]);
+        for (int y = 0; y < h; ++y) {        /* :121-147 */
+            const int yr = imin(y + r, h - 1);
+            for (int x = 0; x < w; ++x) {
+                const int xr = imin(x + r, w - 1);
+                const double q00 = q[(size_t)y * w + x], q10 = q[(size_t)y * w + xr];
+                const double q01 = q[(size_t)yr * w + x], q11 = q[(size_t)yr * w + xr];
+                const double cand[8] = {q00, q10, q01, q11, 0.5 * (q00 + q01), 0.5 * (q10 + q11),
+                                        0.5 * (q00 + q10), 0.5 * (q01 + q11)};
+                const double u = cur[(size_t)y * w + x];
+                double best = cand[0], best_abs = fabs(cand[0] - u);
+                for (int i = 1; i < 8; ++i) {
+                    const double d = fabs(cand[i] - u);
+                    if (d < best_abs) {
+                        best_abs = d;
+                        best = cand[i];
+                    }
+                }
+                nxt[(size_t)y * w + x] = best;
+            }
+        }
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    memcpy(out, cur, sizeof(double) * n);
+    free(cur); free(nxt); free(q); free(c);
+    return ORACLE_OK;
+}

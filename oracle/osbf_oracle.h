@@ -58,6 +58,13 @@ int oracle_osbf(const double* in, double* out, int w, int h, int r, int iteratio
 int oracle_osbf_mt(const double* in, double* out, int w, int h, int r, int iterations,
                    int threads);
 
+/* filters2d.hpp:105-154 (paper Algorithm 3, "fast_osbf"): per iteration one
+ * quarter-mean field Q(x,y) = rect_mean(x-r, y-r, x, y) on the whole-image
+ * SAT, then 8 candidates from the clamped shifted lookups Q(x,y), Q(x+r,y),
+ * Q(x,y+r), Q(x+r,y+r) and their pairwise averages; strict-< first minimum of
+ * |c - u|, output the candidate.  r < 1 is rejected even for 0 iterations. */
+int oracle_fast_osbf(const double* in, double* out, int w, int h, int r, int iterations);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,38 @@ int ref_osbf(const double* in, double* out, int w, int h, int r, int iterations)
     }
 }
 
+// osbf::fast_osbf (filters2d.hpp:105-154, paper Algorithm 3)
+int ref_fast_osbf(const double* in, double* out, int w, int h, int r, int iterations) {
+    try {
+        const auto res = osbf::fast_osbf(to_plane(in, w, h), r, iterations);
+        std::memcpy(out, res.samples().data(), sizeof(double) * res.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// osbf::filter_multichannel with FilterVariant::OsbfFast (filters2d.hpp:371-400).
+int ref_filter_multichannel_fast(const double* in, double* out, int channels, int w, int h, int r,
+                                 int iterations) {
+    try {
+        std::vector<osbf::ImagePlane> planes;
+        for (int c = 0; c < channels; ++c)
+            planes.push_back(to_plane(in + static_cast<size_t>(c) * w * h, w, h));
+        osbf::FilterConfig cfg;
+        cfg.radius = r;
+        cfg.iterations = iterations;
+        cfg.variant = osbf::FilterVariant::OsbfFast;
+        const auto res = osbf::filter_multichannel(osbf::MultiChannelImage(std::move(planes)), cfg);
+        for (int c = 0; c < channels; ++c)
+            std::memcpy(out + static_cast<size_t>(c) * w * h, res.channel(c).samples().data(),
+                        sizeof(double) * static_cast<size_t>(w) * h);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // osbf::osbf_step (filters2d.hpp:61-88)
 int ref_osbf_step(const double* in, double* out, int w, int h, int r) {
     try {

@@ -1,5 +1,5 @@
 """B200-native One-Sided Box Filter (arXiv 2108.05021) — drop-in for the
-reference's exact-OSBF path (osbf::osbf / osbf_step / filter_multichannel).
+reference's OSBF path (osbf::osbf / osbf_step / fast_osbf / filter_multichannel).
 
 The compute lives in ``libosbf_gpu.so`` (hand-written sm_100a CUDA behind the
 C ABI in ``include/osbf_gpu.h``); this package is the Python host side.
@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     SubWindowId,
     build_sat,
     default_context,
+    fast_osbf,
     filter_multichannel,
     max_threads,
     osbf,
@@ -29,7 +30,8 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "build", "lib", "Context", "default_context", "osbf", "osbf_step", "filter_multichannel",
+    "build", "lib", "Context", "default_context", "osbf", "osbf_step", "fast_osbf",
+    "filter_multichannel",
     "build_sat", "subwindow_means", "sub_windows", "SubWindowId", "FilterConfig", "FilterVariant",
     "set_max_threads", "max_threads", "OsbfError", "InvalidArgument", "DomainError", "OutOfRange",
     "CudaError", "NoDevice", "AllocError",

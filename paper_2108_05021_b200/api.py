@@ -15,7 +15,8 @@ reference                              here
 ``subwindow_means`` filters2d.hpp:26   :func:`subwindow_means` (all pixels at once)
 ``osbf_step`` filters2d.hpp:61         :func:`osbf_step`
 ``osbf`` filters2d.hpp:91              :func:`osbf`
-``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact only)
+``fast_osbf`` filters2d.hpp:105        :func:`fast_osbf` (paper Algorithm 3, bit-identical)
+``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact, OsbfFast)
 ``set_max_threads`` parallel.hpp:20    :func:`set_max_threads` (no-op: the GPU
                                         result does not depend on any launch knob)
 =====================================  =============================================
@@ -202,6 +203,26 @@ class Context:
             iterations, _mode_code(mode), ctypes.c_void_p(stream)))
         return ret
 
+    def fast_osbf(self, src, radius: int, iterations: int, out=None, stream=None):
+        """Paper Algorithm 3 (filters2d.hpp:105-154) over a CUDA tensor of shape
+        (H, W) or (B, H, W); bit-identical to the reference's fast_osbf."""
+        import torch
+
+        x, batch, h, w = _as_batch(src)
+        if out is None:
+            out = torch.empty((batch, h, w), dtype=torch.float64, device=x.device)
+            ret = out.view(src.shape)
+        else:
+            ret = out
+            out = out.view(batch, h, w)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        _check(self._lib.osbf_gpu_fast_osbf(
+            self.handle, _dtype_code(x), ctypes.c_void_p(x.data_ptr()), x.stride(1), x.stride(0),
+            ctypes.c_void_p(out.data_ptr()), out.stride(1), out.stride(0), w, h, batch, radius,
+            iterations, ctypes.c_void_p(stream)))
+        return ret
+
     def subwindow_means(self, src, radius: int, mode="exact", stream=None):
         """All-pixel subwindow_means (filters2d.hpp:26-34) and the selection map."""
         import torch
@@ -288,6 +309,23 @@ class Context:
             w, h, batch, radius, iterations, _mode_code(mode)))
         return out
 
+    def fast_osbf_host(self, planes: np.ndarray, radius: int, iterations: int) -> np.ndarray:
+        """fast_osbf on host arrays (H, W) or (B, H, W): copy in, filter, copy out."""
+        p = np.ascontiguousarray(planes)
+        code = {np.dtype(np.uint8): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2}.get(p.dtype)
+        if code is None:
+            p = p.astype(np.float64)
+            code = 2
+        if p.ndim not in (2, 3):
+            raise InvalidArgument("expected a (H, W) or (B, H, W) array")
+        batch = 1 if p.ndim == 2 else p.shape[0]
+        h, w = p.shape[-2:]
+        out = np.empty(p.shape, dtype=np.float64)
+        _check(self._lib.osbf_gpu_fast_osbf_host(
+            self.handle, code, ctypes.c_void_p(p.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+            w, h, batch, radius, iterations))
+        return out
+
     def osbf_step_host(self, plane: np.ndarray, radius: int, mode="exact") -> np.ndarray:
         p = np.ascontiguousarray(plane, dtype=np.float64)
         if p.ndim != 2:
@@ -300,7 +338,7 @@ class Context:
         return out
 
     def filter_multichannel_host(self, channels, radius: int, iterations: int, mode="exact",
-                                 outs=None):
+                                 outs=None, variant: "FilterVariant | None" = None):
         chans = [np.ascontiguousarray(c, dtype=np.float64) for c in channels]
         if not chans:
             raise InvalidArgument("MultiChannelImage: channel count must be in [1,4]")
@@ -312,8 +350,12 @@ class Context:
             outs = [np.empty((h, w), dtype=np.float64) for _ in chans]
         ins = (ctypes.c_void_p * len(chans))(*[c.ctypes.data for c in chans])
         ous = (ctypes.c_void_p * len(chans))(*[o.ctypes.data for o in outs])
-        _check(self._lib.osbf_gpu_filter_multichannel_host(
-            self.handle, ins, ous, len(chans), w, h, radius, iterations, _mode_code(mode)))
+        if variant is FilterVariant.OsbfFast:
+            _check(self._lib.osbf_gpu_filter_multichannel_fast_host(
+                self.handle, ins, ous, len(chans), w, h, radius, iterations))
+        else:
+            _check(self._lib.osbf_gpu_filter_multichannel_host(
+                self.handle, ins, ous, len(chans), w, h, radius, iterations, _mode_code(mode)))
         return outs
 
     def sat_host(self, plane: np.ndarray) -> np.ndarray:
@@ -388,10 +430,19 @@ def osbf_step(plane, r: int, mode="exact"):
     return osbf(plane, r, 1, mode)
 
 
+def fast_osbf(plane, r: int, iterations: int):
+    """filters2d.hpp:105-154 — paper Algorithm 3, bit-identical.  ``r < 1`` or
+    ``iterations < 0`` raise InvalidArgument (the radius even for 0 iterations)."""
+    if _is_tensor(plane):
+        return default_context(plane.device.index or 0).fast_osbf(plane, r, iterations)
+    return default_context().fast_osbf_host(np.asarray(plane), r, iterations)
+
+
 def filter_multichannel(channels, config: FilterConfig, mode="exact"):
-    """filters2d.hpp:371-400, OsbfExact branch: channels filtered independently."""
+    """filters2d.hpp:371-400, OsbfExact and OsbfFast branches: channels
+    filtered independently (one batched launch per pass)."""
     config.validate()
-    if config.variant is not FilterVariant.OsbfExact:
+    if config.variant not in (FilterVariant.OsbfExact, FilterVariant.OsbfFast):
         raise InvalidArgument(
             f"filter_multichannel: variant {config.variant.name} is not on the GPU OSBF path")
     chans = list(channels) if not (hasattr(channels, "ndim") and channels.ndim == 3) else channels
@@ -401,10 +452,12 @@ def filter_multichannel(channels, config: FilterConfig, mode="exact"):
         import torch
 
         stack = chans if _is_tensor(chans) else torch.stack(list(chans))
-        return default_context(stack.device.index or 0).iterate(
-            stack, config.radius, config.iterations, mode)
+        ctx = default_context(stack.device.index or 0)
+        if config.variant is FilterVariant.OsbfFast:
+            return ctx.fast_osbf(stack, config.radius, config.iterations)
+        return ctx.iterate(stack, config.radius, config.iterations, mode)
     return default_context().filter_multichannel_host(chans, config.radius, config.iterations,
-                                                      mode)
+                                                      mode, variant=config.variant)
 
 
 def build_sat(plane):

@@ -205,6 +205,64 @@ cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, 
 }
 }  // namespace osbf_gpu
 
+namespace {
+
+// Jacobi ping-pong through context scratch (filters2d.hpp:94-97 / :112-152:
+// every iteration reads the previous plane and writes a fresh one); the last
+// launch writes d_out.  want(remaining) is the number of passes (1 or 2) the
+// next launch should run; run(src, dst, dst_pitch, dst_plane, n, &retry)
+// launches them, setting retry when n = 2 has no kernel (then one pass).
+template <typename Want, typename Run>
+osbf_status jacobi(osbf_ctx* ctx, const osbf_gpu::PlaneView& input, const osbf_gpu::Geometry& g,
+                   int iterations, double* d_out, size_t out_pitch, size_t out_plane,
+                   cudaStream_t s, Want&& want, Run&& run) {
+    const size_t plane = static_cast<size_t>(g.width) * g.height;
+    const bool alias = static_cast<const void*>(d_out) == input.base;
+    const int scratch_needed = (iterations > 1 ? 2 : 0) + (alias ? 1 : 0);
+    if (scratch_needed > 0) OSBF_CUDA(ctx->ping.ensure(plane * g.batch * sizeof(double)), "alloc ping");
+    if (scratch_needed > 1) OSBF_CUDA(ctx->pong.ensure(plane * g.batch * sizeof(double)), "alloc pong");
+    osbf_gpu::PlaneView src = input;
+    int done = 0;
+    for (int k = 0; done < iterations; ++k) {
+        int n = want(iterations - done);
+        for (;;) {
+            const bool last = done + n == iterations;
+            double* dst;
+            size_t dp, dpl;
+            if (last && !alias) {
+                dst = d_out;
+                dp = out_pitch;
+                dpl = out_plane;
+            } else {
+                DevBuf& buf = (k % 2 == 0) ? ctx->ping : ctx->pong;
+                dst = buf.as<double>();
+                dp = g.width;
+                dpl = plane;
+            }
+            bool retry = false;
+            const osbf_status st = run(src, dst, dp, dpl, n, &retry);
+            if (retry && n == 2) {
+                n = 1;
+                continue;
+            }
+            if (st != OSBF_OK) return st;
+            src = osbf_gpu::PlaneView{dst, OSBF_F64, dp, dpl};
+            break;
+        }
+        done += n;
+    }
+    if (alias) {
+        OSBF_CUDA(cudaMemcpy2DAsync(d_out, out_pitch * sizeof(double), src.base,
+                                    src.pitch * sizeof(double), g.width * sizeof(double),
+                                    static_cast<size_t>(g.height) * g.batch,
+                                    cudaMemcpyDeviceToDevice, s),
+                  "copy back");
+    }
+    return OSBF_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int osbf_gpu_abi_version(void) { return OSBF_GPU_ABI_VERSION; }
@@ -300,57 +358,67 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
                   "copy");
         return OSBF_OK;
     }
-    // Jacobi ping-pong through context scratch; the last pass writes d_out.
-    const size_t plane = static_cast<size_t>(width) * height;
-    const bool alias = static_cast<const void*>(d_out) == d_in;
-    const int scratch_needed = (iterations > 1 ? 2 : 0) + (alias ? 1 : 0);
-    if (scratch_needed > 0) OSBF_CUDA(ctx->ping.ensure(plane * batch * sizeof(double)), "alloc ping");
-    if (scratch_needed > 1) OSBF_CUDA(ctx->pong.ensure(plane * batch * sizeof(double)), "alloc pong");
-    osbf_gpu::PlaneView src = input;
-    int done = 0;
-    for (int step = 0; done < iterations; ++step) {
-        // Fast mode runs two passes per launch (temporal blocking) when the
-        // radius has a two-pass kernel; otherwise one pass per launch.
-        const bool tb2 = ctx->passes_per_launch == 2 || tb2_env();
-        int npass = (mode == OSBF_MODE_FAST && iterations - done >= 2 && tb2) ? 2 : 1;
-        for (;;) {
-            const bool last = done + npass == iterations;
-            double* dst;
-            size_t dp, dpl;
-            if (last && !alias) {
-                dst = d_out;
-                dp = out_pitch;
-                dpl = out_plane_stride;
-            } else {
-                DevBuf& buf = (step % 2 == 0) ? ctx->ping : ctx->pong;
-                dst = buf.as<double>();
-                dp = width;
-                dpl = plane;
-            }
-            if (npass == 2) {
+    // Fast mode runs two passes per launch (temporal blocking) when enabled
+    // and the radius has a two-pass kernel; otherwise one pass per launch.
+    const bool tb2 = mode == OSBF_MODE_FAST && (ctx->passes_per_launch == 2 || tb2_env());
+    return jacobi(
+        ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, s,
+        [&](int remaining) { return tb2 && remaining >= 2 ? 2 : 1; },
+        [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int n,
+            bool* retry) -> osbf_status {
+            if (n == 2) {
                 const cudaError_t e = osbf_gpu::fast_step2(src, g, radius, dst, dp, dpl, s, ctx->lc);
                 if (e == cudaErrorNotSupported) {
                     cudaGetLastError();
-                    npass = 1;
-                    continue;
+                    *retry = true;
+                    return OSBF_OK;
                 }
                 OSBF_CUDA(e, "fast two-pass step");
-            } else if ((st = one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s)) !=
-                       OSBF_OK) {
-                return st;
+                return OSBF_OK;
             }
-            src = osbf_gpu::PlaneView{dst, OSBF_F64, dp, dpl};
-            done += npass;
-            break;
-        }
+            return one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s);
+        });
+}
+
+osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                              size_t in_pitch, size_t in_plane_stride, double* d_out,
+                              size_t out_pitch, size_t out_plane_stride, int width, int height,
+                              int batch, int radius, int iterations, void* stream) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    // filters2d.hpp:107-110: the radius is checked first, even for 0 iterations
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: radius must be >= 1");
+    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: iterations must be >= 0");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if (!d_in || !d_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null plane pointer");
+    if (in_pitch < static_cast<size_t>(width) || out_pitch < static_cast<size_t>(width))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "pitch smaller than width");
+    if (batch > 1 && (in_plane_stride < in_pitch * height || out_plane_stride < out_pitch * height))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "plane stride smaller than pitch*height");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = pick_stream(ctx, stream);
+    const osbf_gpu::Geometry g{width, height, batch};
+    const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_plane_stride};
+    if (iterations == 0) {
+        if (static_cast<const void*>(d_out) == d_in && in_dtype == OSBF_F64) return OSBF_OK;
+        OSBF_CUDA(osbf_gpu::convert_to_f64(input, g, d_out, out_pitch, out_plane_stride, s, ctx->lc),
+                  "copy");
+        return OSBF_OK;
     }
-    if (alias) {
-        OSBF_CUDA(cudaMemcpy2DAsync(d_out, out_pitch * sizeof(double), src.base,
-                                    src.pitch * sizeof(double), width * sizeof(double),
-                                    static_cast<size_t>(height) * batch, cudaMemcpyDeviceToDevice, s),
-                  "copy back");
-    }
-    return OSBF_OK;
+    const size_t n = static_cast<size_t>(batch) * width * height;
+    const size_t ns = static_cast<size_t>(batch) * (width + 1) * (height + 1);
+    OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");
+    OSBF_CUDA(ctx->sat.ensure(ns * sizeof(double)), "alloc sat");
+    return jacobi(
+        ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, s, [](int) { return 1; },
+        [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int,
+            bool*) -> osbf_status {
+            OSBF_CUDA(osbf_gpu::fastosbf_pass(src, g, radius, ctx->rowpfx.as<double>(),
+                                              ctx->sat.as<double>(), dst, dp, dpl, s, ctx->lc),
+                      "fast_osbf pass");
+            return OSBF_OK;
+        });
 }
 
 osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
@@ -454,16 +522,16 @@ osbf_status osbf_gpu_step_band_push(osbf_ctx* ctx, osbf_dtype in_dtype, const vo
     return OSBF_OK;
 }
 
-osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
-                               double* h_out, int width, int height, int batch, int radius,
-                               int iterations, osbf_mode mode) {
-    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
-    osbf_status st;
-    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
-    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
-    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf: iterations must be >= 0");
-    if (iterations > 0 && radius < 1)
-        return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+}  // extern "C"
+
+namespace {
+// Host-buffer batch: H2D, filter(d_in, d_out, planes) on the compute stream,
+// D2H.  Large batches run in chunks so the upload of chunk j+1 and the
+// download of chunk j-1 (two copy streams) overlap the passes of chunk j.
+template <typename Filter>
+osbf_status host_batch(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in, double* h_out,
+                       int width, int height, int batch, Filter&& filter) {
+    osbf_status st = OSBF_OK;
     if (!h_in || !h_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
     OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     const size_t n = static_cast<size_t>(width) * height * batch;
@@ -484,8 +552,7 @@ osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h
     if (chunks == 1) {
         OSBF_CUDA(cudaMemcpyAsync(din, hin, n * dtype_size(in_dtype), cudaMemcpyHostToDevice, s),
                   "H2D");
-        st = osbf_gpu_iterate(ctx, in_dtype, din, width, plane, dout, width, plane, width, height,
-                              batch, radius, iterations, mode, s);
+        st = filter(din, dout, batch);
         if (st != OSBF_OK) return st;
         OSBF_CUDA(cudaMemcpyAsync(h_out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, s),
                   "D2H");
@@ -520,8 +587,7 @@ osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h
             st = cuda_fail(e, "H2D");
             break;
         }
-        st = osbf_gpu_iterate(ctx, in_dtype, din + b0 * in_bytes, width, plane, dout + b0 * plane,
-                              width, plane, width, height, b1 - b0, radius, iterations, mode, s);
+        st = filter(din + b0 * in_bytes, dout + b0 * plane, b1 - b0);
         if (st != OSBF_OK) break;
         e = cudaEventRecord(ev[2 * j + 1], s);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy_out, ev[2 * j + 1], 0);
@@ -541,16 +607,61 @@ osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h
     return OSBF_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                               double* h_out, int width, int height, int batch, int radius,
+                               int iterations, osbf_mode mode) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf: iterations must be >= 0");
+    if (iterations > 0 && radius < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
+    const size_t plane = static_cast<size_t>(width) * height;
+    return host_batch(ctx, in_dtype, h_in, h_out, width, height, batch,
+                      [&](const void* din, double* dout, int nb) {
+                          return osbf_gpu_iterate(ctx, in_dtype, din, width, plane, dout, width,
+                                                  plane, width, height, nb, radius, iterations,
+                                                  mode, ctx->stream);
+                      });
+}
+
+osbf_status osbf_gpu_fast_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                                    double* h_out, int width, int height, int batch, int radius,
+                                    int iterations) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: radius must be >= 1");
+    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: iterations must be >= 0");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    const size_t plane = static_cast<size_t>(width) * height;
+    return host_batch(ctx, in_dtype, h_in, h_out, width, height, batch,
+                      [&](const void* din, double* dout, int nb) {
+                          return osbf_gpu_fast_osbf(ctx, in_dtype, din, width, plane, dout, width,
+                                                    plane, width, height, nb, radius, iterations,
+                                                    ctx->stream);
+                      });
+}
+
 osbf_status osbf_gpu_osbf_step_host(osbf_ctx* ctx, const double* h_in, double* h_out, int width,
                                     int height, int radius, osbf_mode mode) {
     if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
     return osbf_gpu_osbf_host(ctx, OSBF_F64, h_in, h_out, width, height, 1, radius, 1, mode);
 }
 
-osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const* h_in,
-                                              double* const* h_out, int channels, int width,
-                                              int height, int radius, int iterations,
-                                              osbf_mode mode) {
+}  // extern "C"
+
+namespace {
+// filter_multichannel (filters2d.hpp:371-400) for either variant: channels
+// are independent, so they run as one batched launch per pass.
+osbf_status multichannel_host(osbf_ctx* ctx, const double* const* h_in, double* const* h_out,
+                              int channels, int width, int height, int radius, int iterations,
+                              bool fast_variant, osbf_mode mode) {
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
     // FilterConfig::validate (core.hpp:244-253), then the channel checks of
     // MultiChannelImage (core.hpp:85-92).
@@ -576,8 +687,10 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
                   "H2D");
     }
     // Channels are independent (filters2d.hpp:376-384): one batched launch.
-    st = osbf_gpu_iterate(ctx, OSBF_F64, din, width, plane, dout, width, plane, width, height,
-                          channels, radius, iterations, mode, s);
+    st = fast_variant ? osbf_gpu_fast_osbf(ctx, OSBF_F64, din, width, plane, dout, width, plane,
+                                           width, height, channels, radius, iterations, s)
+                      : osbf_gpu_iterate(ctx, OSBF_F64, din, width, plane, dout, width, plane,
+                                         width, height, channels, radius, iterations, mode, s);
     if (st != OSBF_OK) return st;
     for (int c = 0; c < channels; ++c)
         OSBF_CUDA(cudaMemcpyAsync(h_out[c], dout + c * plane, plane * sizeof(double),
@@ -585,6 +698,25 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
                   "D2H");
     OSBF_CUDA(cudaStreamSynchronize(s), "sync");
     return OSBF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const* h_in,
+                                              double* const* h_out, int channels, int width,
+                                              int height, int radius, int iterations,
+                                              osbf_mode mode) {
+    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, false,
+                             mode);
+}
+
+osbf_status osbf_gpu_filter_multichannel_fast_host(osbf_ctx* ctx, const double* const* h_in,
+                                                   double* const* h_out, int channels, int width,
+                                                   int height, int radius, int iterations) {
+    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, true,
+                             OSBF_MODE_EXACT);
 }
 
 osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,

@@ -1,0 +1,105 @@
+// Paper Algorithm 3, the reference's fast_osbf (filters2d.hpp:105-154),
+// bit-identical.  Per iteration:
+//   1. the whole-image summed-area table in the reference's serial order
+//      (exact_build_sat, the same kernels the exact OSBF diagnostics use);
+//   2. fosbf_quarter: Q(x,y) = rect_mean(x-r, y-r, x, y) (filters2d.hpp:116-
+//      119): clipped ((A-B)-C)+D, one IEEE division by the clipped count
+//      (integral.hpp:41-69), written over the row-prefix workspace (free once
+//      the table exists);
+//   3. fosbf_select: the four clamped shifted quarters, the four pairwise
+//      averages 0.5*(a+b) in the reference's order, strict-< first minimum of
+//      |c - u|, write the candidate (filters2d.hpp:121-147).
+// Every fp64 operation is an _rn intrinsic, so nothing is contracted.
+#include "osbf_internal.cuh"
+
+namespace osbf_gpu {
+namespace {
+
+__global__ void __launch_bounds__(256)
+    fosbf_quarter(const double* __restrict__ sat, double* __restrict__ q, int W, int H, int r) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int b = blockIdx.z;
+    if (x >= W || y >= H) return;
+    const long long cols = static_cast<long long>(W) + 1;
+    const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
+    const int x0 = max(x - r, 0), y0 = max(y - r, 0);  // x1 = x, y1 = y are in range
+    const long long n = static_cast<long long>(x - x0 + 1) * (y - y0 + 1);
+    const double A = C[(y + 1) * cols + (x + 1)];
+    const double Bv = C[(y + 1) * cols + x0];
+    const double Cv = C[y0 * cols + (x + 1)];
+    const double D = C[y0 * cols + x0];
+    const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
+    q[(static_cast<size_t>(b) * H + y) * W + x] = __ddiv_rn(s, static_cast<double>(n));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    fosbf_select(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
+                 const double* __restrict__ q, double* __restrict__ out, size_t out_pitch,
+                 size_t out_plane, int W, int H, int r) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int b = blockIdx.z;
+    if (x >= W || y >= H) return;
+    const double* Q = q + static_cast<size_t>(b) * H * W;
+    const int yr = min(y + r, H - 1), xr = min(x + r, W - 1);
+    const double q00 = Q[static_cast<size_t>(y) * W + x];
+    const double q10 = Q[static_cast<size_t>(y) * W + xr];
+    const double q01 = Q[static_cast<size_t>(yr) * W + x];
+    const double q11 = Q[static_cast<size_t>(yr) * W + xr];
+    const double cand[8] = {q00,
+                            q10,
+                            q01,
+                            q11,
+                            __dmul_rn(0.5, __dadd_rn(q00, q01)),   // left half
+                            __dmul_rn(0.5, __dadd_rn(q10, q11)),   // right half
+                            __dmul_rn(0.5, __dadd_rn(q00, q10)),   // upper half
+                            __dmul_rn(0.5, __dadd_rn(q01, q11))};  // lower half
+    const double u = to_f64(in[b * in_plane + static_cast<size_t>(y) * in_pitch + x]);
+    double best = cand[0];
+    double best_abs = fabs(__dsub_rn(cand[0], u));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        const double d = fabs(__dsub_rn(cand[i], u));
+        if (d < best_abs) {
+            best_abs = d;
+            best = cand[i];
+        }
+    }
+    out[b * out_plane + static_cast<size_t>(y) * out_pitch + x] = best;
+}
+
+}  // namespace
+
+cudaError_t fastosbf_pass(const PlaneView& in, const Geometry& g, int radius, double* rowpfx,
+                          double* sat, double* out, size_t out_pitch, size_t out_plane,
+                          cudaStream_t s, LaunchCounter& lc) {
+    cudaError_t e = exact_build_sat(in, g, rowpfx, sat, s, lc);
+    if (e != cudaSuccess) return e;
+    const dim3 grid((g.width + 31) / 32, (g.height + 7) / 8, g.batch);
+    fosbf_quarter<<<grid, 256, 0, s>>>(sat, rowpfx, g.width, g.height, radius);
+    ++lc.launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++lc.launches;
+    switch (in.dtype) {
+        case OSBF_U8:
+            fosbf_select<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(in.base), in.pitch,
+                                              in.plane, rowpfx, out, out_pitch, out_plane,
+                                              g.width, g.height, radius);
+            break;
+        case OSBF_F32:
+            fosbf_select<<<grid, 256, 0, s>>>(static_cast<const float*>(in.base), in.pitch,
+                                              in.plane, rowpfx, out, out_pitch, out_plane,
+                                              g.width, g.height, radius);
+            break;
+        default:
+            fosbf_select<<<grid, 256, 0, s>>>(static_cast<const double*>(in.base), in.pitch,
+                                              in.plane, rowpfx, out, out_pitch, out_plane,
+                                              g.width, g.height, radius);
+            break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace osbf_gpu

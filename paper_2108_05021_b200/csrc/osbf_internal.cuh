@@ -70,6 +70,14 @@ cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius,
                              double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
                              LaunchCounter& lc);
 
+// ---- paper Algorithm 3 (osbf_fastosbf.cu) ----------------------------------
+// One fast_osbf iteration (filters2d.hpp:105-154), bit-identical: exact SAT
+// into rowpfx/sat (rowpfx: [batch][height][width], reused for the quarter
+// field), then quarter means and the candidate selection into out.
+cudaError_t fastosbf_pass(const PlaneView& in, const Geometry& g, int radius, double* rowpfx,
+                          double* sat, double* out, size_t out_pitch, size_t out_plane,
+                          cudaStream_t s, LaunchCounter& lc);
+
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
 // Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
 constexpr int kFastMaxRadius = 16;

@@ -46,6 +46,10 @@ def golden_cases():
                   if not p.endswith("sat_2x2.npz"))
 
 
+def fastosbf_golden_cases():
+    return sorted(glob.glob(os.path.join(GOLDEN_DIR, "fastosbf", "*.npz")))
+
+
 def load_golden(path):
     d = np.load(path)
     return {k: d[k] for k in d.files}

@@ -233,6 +233,39 @@ int main() {
         return true;
     });
 
+    // ---- fast_osbf (paper Algorithm 3): test_filters2d.cpp:169-186 + errors
+    run("fast_osbf keeps constant planes and ideal steps", [] {
+        const ImagePlane c(9, 9, 11.0);
+        if (max_abs_diff(osbf::fast_osbf(c, 3, 2), c) != 0.0) return false;
+        for (int r : {1, 2, 5}) {
+            const auto p = step(32, 16, 16, 0.0, 100.0);
+            if (max_abs_diff(osbf::fast_osbf(p, r, 1), p) != 0.0) return false;
+        }
+        return true;
+    });
+    run("fast_osbf bit-identical to the oracle; errors as the reference", [] {
+        for (int r : {1, 2, 3, 7}) {
+            const auto p = random_plane(41, 27, 300 + r);
+            std::vector<double> want(p.size());
+            if (oracle_fast_osbf(p.samples().data(), want.data(), 41, 27, r, 4) != 0) return false;
+            const auto got = osbf::fast_osbf(p, r, 4);
+            if (std::memcmp(got.samples().data(), want.data(), sizeof(double) * want.size()) != 0)
+                return false;
+        }
+        const auto p = random_plane(8, 8, 1);
+        osbf::FilterConfig cfg;
+        cfg.radius = 2;
+        cfg.iterations = 3;
+        cfg.variant = osbf::FilterVariant::OsbfFast;
+        const osbf::MultiChannelImage rgb({random_plane(12, 10, 4), random_plane(12, 10, 5)});
+        const auto out = osbf::filter_multichannel(rgb, cfg);
+        for (int c = 0; c < 2; ++c)
+            if (!bit_equal(out.channel(c), osbf::fast_osbf(rgb.channel(c), 2, 3))) return false;
+        return throws<std::invalid_argument>([&] { osbf::fast_osbf(p, 0, 0); }) &&
+               throws<std::invalid_argument>([&] { osbf::fast_osbf(p, 2, -1); }) &&
+               bit_equal(osbf::fast_osbf(p, 2, 0), p);
+    });
+
     // ---- acceptance.cpp criteria 1, 2, 5
     run("acceptance 1: edge fixed point (256^2, r in {1,2,5,10}, 30 it)", [] {
         double worst = 0.0;

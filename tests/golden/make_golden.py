@@ -76,6 +76,30 @@ def cases():
     return out
 
 
+def fast_osbf_cases():
+    """(name, input, r, iterations) for fast_osbf (filters2d.hpp:105-154)."""
+    out = []
+    # test_filters2d.cpp:169-177 — constant plane and ideal steps are fixed points
+    out.append(("constant_9x9_r3", np.full((9, 9), 11.0), 3, 2))
+    for r in (1, 2, 5):
+        out.append((f"step_32x16_r{r}", step(32, 16, 16, 0.0, 100.0), r, 1))
+    # test_filters2d.cpp:179-186 / acceptance.cpp:106-134 — a structured image
+    # (seeded mosaic + noise stands in for the reference's phantom fixture)
+    ph = synth.make_input("C1", shrink=4)[0].astype(np.float64) * 255.0
+    for r in (2, 6):
+        out.append((f"mosaic128_r{r}", ph, r, 10))
+    for r in (1, 3, 7, 16):
+        out.append((f"random_50x37_r{r}", random_plane(37, 50, 300 + r), r, 4))
+    rng = np.random.default_rng(34)
+    out.append(("u8mosaic_r4", synth.u8_mosaic(96, 80, rng, block=(4, 40)), 4, 10))
+    out.append(("one_px", np.array([[7.5]]), 2, 3))
+    out.append(("row_1x17", random_plane(1, 17, 15), 3, 2))
+    out.append(("col_13x1", random_plane(13, 1, 16), 2, 2))
+    out.append(("zero_iters", random_plane(10, 10, 13), 2, 0))
+    out.append(("c2_shrink12", synth.make_input("C2", shrink=12), 3, 5))
+    return out
+
+
 def main() -> None:
     ref = Reference()
     ref.set_max_threads(1)
@@ -90,6 +114,14 @@ def main() -> None:
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), input=inp, output=out,
                             radius=r, iterations=iters, step1_sel=sel, **extra)
         print(f"{name:24s} in {inp.shape} {inp.dtype} r={r} it={iters}")
+    os.makedirs(os.path.join(HERE, "fastosbf"), exist_ok=True)
+    for name, inp, r, iters in fast_osbf_cases():
+        x = inp.astype(np.float64)
+        out = (ref.filter_multichannel(x, r, iters, variant="fast") if x.ndim == 3
+               else ref.fast_osbf(x, r, iters))
+        np.savez_compressed(os.path.join(HERE, "fastosbf", f"{name}.npz"), input=inp, output=out,
+                            radius=r, iterations=iters)
+        print(f"fastosbf/{name:20s} in {inp.shape} {inp.dtype} r={r} it={iters}")
     # integral.hpp / test_integral.cpp:19-29 known SAT
     p = np.array([[1.0, 2.0], [3.0, 4.0]])
     np.savez_compressed(os.path.join(HERE, "sat_2x2.npz"), input=p, cumsum=ref.sat(p))

@@ -1,5 +1,6 @@
 """Quick per-pass timing of the OSBF kernels (CUDA events, warm, L2-flushed).
-usage: python tools/prof_pass.py [--mode fast|exact] [--radii 1,2,4,8,16] [--shape B,H,W]"""
+usage: python tools/prof_pass.py [--mode fast|exact|fastosbf] [--radii 1,2,4,8,16] [--shape B,H,W]
+(fastosbf = paper Algorithm 3, osbf_gpu_fast_osbf)"""
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -18,13 +19,15 @@ y = torch.empty_like(x)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 for r in map(int, a.radii.split(",")):
+    run = ((lambda: ctx.fast_osbf(x, r, 1, out=y)) if a.mode == "fastosbf"
+           else (lambda: ctx.iterate(x, r, 1, mode=a.mode, out=y)))
     for _ in range(3):
-        ctx.iterate(x, r, 1, mode=a.mode, out=y)
+        run()
     ts = []
     for _ in range(a.reps):
         flush.fill_(1)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(); ctx.iterate(x, r, 1, mode=a.mode, out=y); e.record()
+        s.record(); run(); e.record()
         torch.cuda.synchronize(); ts.append(s.elapsed_time(e))
     ts.sort(); ms = ts[len(ts) // 2]
     px = B * H * W
