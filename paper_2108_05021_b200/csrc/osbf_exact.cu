@@ -214,10 +214,22 @@ cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carri
         cudaError_t e = cudaFuncSetAttribute(ex2::exact_row_carries<T>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(ex2::K1_SMEM));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(ex2::K1D_SMEM));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const long long rows = static_cast<long long>(g.batch) * g.height;
+    const long long warps = (rows + 31) / 32;
+    if (warps <= 2 * 148) {  // about one warp per SM: deep single-warp CTAs
+        ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>
+            <<<static_cast<unsigned>(warps), 32, ex2::K1D_SMEM, s>>>(
+                static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height,
+                rows, nsc);
+        return cudaGetLastError();
+    }
     const long long ctas = (rows + ex2::NTK1 - 1) / ex2::NTK1;
     ex2::exact_row_carries<T><<<static_cast<unsigned>(ctas), ex2::NTK1, ex2::K1_SMEM, s>>>(
         static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height, rows, nsc);

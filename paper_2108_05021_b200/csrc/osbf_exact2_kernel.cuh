@@ -69,7 +69,7 @@ constexpr int BR = 32;   // rows per block
 constexpr int NT = 256;  // threads per strip CTA
 constexpr int NTK1 = 64; // threads per carry CTA (2 warps, 32 rows each)
 
-template <int R>
+template <int R, int NUBV = 3>
 struct XLay {
     // staged U columns: [xs, xs + NU) with xs = floor((X0-R)/SW)*SW >= X0-R-SW+1,
     // covering up to X0 + TW + R - 1
@@ -85,11 +85,13 @@ struct XLay {
     // row segments of SW columns between stored carries (RR parallelism)
     static constexpr int NSEGR = (NU + SW - 1) / SW;
     static_assert(NSEGR * BR <= NT, "row segments exceed the CTA");
-    // U buffers in flight: S(k-1), block k, RR(k+1); block k+2 is staged
-    // into S(k-1)'s buffer after iteration k's last barrier
-    static constexpr int NUB = 3;
+    // U (+ carry) buffers: S(k-1), block k, RR(k+1) and NUB-3 more blocks in
+    // flight; block k+NUB-1 is staged into S(k-1)'s buffer after iteration
+    // k's last barrier.  The stencil strips use 3; the carries pass (no
+    // stencil, short iterations) stages deeper to cover DRAM latency.
+    static constexpr int NUB = NUBV;
     static constexpr size_t SMEM = sizeof(double) * (NUB * static_cast<size_t>(U_ELEMS) + BR * PR +
-                                                     NRING * NCC + 2 * BR * NSEGR);
+                                                     NRING * NCC + NUB * BR * NSEGR);
     // warps: column chains on [0, CCW), the early stencil rows on the rest;
     // row prefixes on [0, RRW), the late stencil rows on the rest
     static constexpr int CCW = (NCC + 31) / 32;
@@ -123,13 +125,18 @@ __device__ __forceinline__ void cp_wait() {
 constexpr int K1_STAGES = 3;
 constexpr size_t K1_SMEM = sizeof(double) * (NTK1 / 32) * K1_STAGES * 32 * 33;
 
-template <typename T>
-__global__ void __launch_bounds__(NTK1)
+// Few rows (one plane): one warp per CTA with a deep ring, so each SM's
+// single warp keeps ~8 chunks of loads in flight across the DRAM latency.
+constexpr int K1D_STAGES = 8;
+constexpr size_t K1D_SMEM = sizeof(double) * K1D_STAGES * 32 * 33;
+
+template <typename T, int WARPS = NTK1 / 32, int K1_STAGES = ex2::K1_STAGES>
+__global__ void __launch_bounds__(WARPS * 32)
     exact_row_carries(const T* __restrict__ in, size_t pitch, size_t plane,
                       double* __restrict__ carries, int W, int H, long long rows, int nsc) {
     extern __shared__ double k1s[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long row0 = (static_cast<long long>(blockIdx.x) * (NTK1 / 32) + warp) * 32;
+    const long long row0 = (static_cast<long long>(blockIdx.x) * WARPS + warp) * 32;
     if (row0 >= rows) return;
     double* ring = k1s + static_cast<size_t>(warp) * K1_STAGES * 32 * 33;
     long long my_base = -1;
@@ -227,11 +234,14 @@ __device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pi
             }
         }
     }
-    // carries R(xs + 16*seg - 1, y) for the row segments (cs[seg*BR + row])
+    // carries R(xs + 16*seg - 1, y) for the row segments (cs[seg*BR + row]),
+    // asynchronously like the samples (a plain load here would hold the
+    // issuing warps for a full DRAM latency before the next barrier)
     if (threadIdx.x < BR * L::NSEGR) {
         const int rr = threadIdx.x % BR, seg = threadIdx.x / BR;
         const int y = y0 + rr;
-        cs[threadIdx.x] = (y < H && s0 + seg < nsc) ? carries[(gbase + y) * nsc + s0 + seg] : 0.0;
+        const bool ok = y < H && s0 + seg < nsc;
+        cp_async8(cs + threadIdx.x, carries + (ok ? (gbase + y) * nsc + s0 + seg : 0), ok);
     }
     cp_commit();
 }
@@ -352,12 +362,13 @@ __global__ void __launch_bounds__(NT, 2)
                 const double* __restrict__ carries, int nsc, double* __restrict__ out,
                 size_t opitch, size_t oplane, int W, int H, int band_h,
                 double* __restrict__ ccar) {
-    using L = XLay<R>;
+    using L = XLay<R, CARRIES ? 6 : 3>;
+    constexpr int AHEAD = L::NUB - 2;  // blocks staged ahead of the row prefixes
     extern __shared__ double sm[];
     double* Ubuf = sm;                          // NUB x [BR][PUB]
     double* Rb = sm + L::NUB * L::U_ELEMS;      // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
     double* Cr = Rb + BR * L::PR;               // [NRING][NCC]: table rows, column cx = X0-R+t
-    double* cs = Cr + L::NRING * L::NCC;        // 2 x [NSEGR][BR] staged carries
+    double* cs = Cr + L::NRING * L::NCC;        // NUB x [NSEGR][BR] staged carries
     const int b = blockIdx.y;
     const int X0 = blockIdx.x * TW;
     const int xs_raw = X0 - R;
@@ -386,7 +397,14 @@ __global__ void __launch_bounds__(NT, 2)
     const bool aligned16 = sizeof(T) == 8 && (pitch % 2 == 0) &&
                            (reinterpret_cast<uintptr_t>(src) % 16 == 0);
     auto U_of = [&](int k) { return Ubuf + (k % L::NUB) * L::U_ELEMS; };
-    auto cs_of = [&](int k) { return cs + (k & 1) * BR * L::NSEGR; };
+    auto cs_of = [&](int k) { return cs + (k % L::NUB) * BR * L::NSEGR; };
+    auto stage = [&](int k) {  // block k, or an empty group past the end
+        if (k < nblocks)
+            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + k * BR, W, H,
+                              U_of(k), cs_of(k), aligned16);
+        else
+            cp_commit();
+    };
 
     // RR: continue the row running sums of block k from the stored carries,
     // one SW-column segment per thread (each segment starts from the exact
@@ -423,13 +441,10 @@ __global__ void __launch_bounds__(NT, 2)
         unsafe = !table_value_safe(creg);
         Cr[ring_row<R>(y_walk0) * L::NCC + tid] = creg;  // table row y_walk0 (zero border at 0)
     }
-    stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0, W, H, U_of(0), cs_of(0),
-                      aligned16);
+    stage(0);
     cp_wait<0>();
     __syncthreads();
-    if (nblocks > 1)  // lands during iteration 0's phase A
-        stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + BR, W, H, U_of(1),
-                          cs_of(1), aligned16);
+    for (int j = 1; j <= AHEAD; ++j) stage(j);  // land during the first iterations
     row_prefix(0);
     __syncthreads();
     const int early = BR - R - 1 > 0 ? BR - R - 1 : 0;  // rows of block k-1 not needing block k
@@ -476,7 +491,7 @@ __global__ void __launch_bounds__(NT, 2)
         } else if (!CARRIES && k > 0) {
             stencil_part(k - 1, 0, early, L::CCW, NT / 32 - L::CCW, safe_prev);
         }
-        cp_wait<0>();  // block k+1 staged
+        cp_wait<AHEAD - 1>();  // block k+1 staged
         unsafe = __syncthreads_or(unsafe);  // sticky for the strip
         // Phase B: row prefixes of block k+1  ||  the last R+1 rows of block k-1
         if (warp < L::RRW) {
@@ -485,10 +500,8 @@ __global__ void __launch_bounds__(NT, 2)
             stencil_part(k - 1, early, BR, L::RRW, NT / 32 - L::RRW, !unsafe);
         }
         __syncthreads();
-        // block k+2 into the buffer S(k-1) just released; lands during k+1
-        if (k + 2 < nblocks)
-            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y0 + 2 * BR, W, H,
-                              U_of(k + 2), cs_of(k + 2), aligned16);
+        // block k+AHEAD+1 into the buffer S(k-1) just released
+        stage(k + AHEAD + 1);
     }
     if (!CARRIES) stencil_part(nblocks - 1, 0, BR, 0, NT / 32, !unsafe);
 }
@@ -500,7 +513,8 @@ template <int R>
 cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double* carries,
                                  int nsc, double* out, size_t opitch, size_t oplane, int band_h,
                                  double* ccar, cudaStream_t s) {
-    using L = ex2::XLay<R>;
+    using L = ex2::XLay<R>;      // stencil strips
+    using LC = ex2::XLay<R, 6>;  // carries pass (deeper staging)
     const int strips = (g.width + ex2::TW - 1) / ex2::TW;
     const int nbands = band_h > 0 ? (g.height + band_h - 1) / band_h : 1;
     auto go = [&](auto tag) -> cudaError_t {
@@ -513,13 +527,13 @@ cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double*
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(ex2::exact_strip<R, T, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(L::SMEM));
+                                         static_cast<int>(LC::SMEM));
             if (e != cudaSuccess) return e;
             configured = true;
         }
         const T* base = static_cast<const T*>(in.base);
         if (nbands > 1) {
-            ex2::exact_strip<R, T, true><<<dim3(strips, g.batch, 1), ex2::NT, L::SMEM, s>>>(
+            ex2::exact_strip<R, T, true><<<dim3(strips, g.batch, 1), ex2::NT, LC::SMEM, s>>>(
                 base, in.pitch, in.plane, carries, nsc, out, opitch, oplane, g.width, g.height,
                 band_h, ccar);
             cudaError_t e = cudaGetLastError();
