@@ -11,6 +11,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "osbf_internal.cuh"
 
@@ -71,6 +72,15 @@ struct DevBuf {
 
 }  // namespace
 
+// One captured launch sequence (a whole multi-pass call) and what it was
+// captured for: every argument and every scratch buffer it touches.
+struct GraphEntry {
+    std::vector<uintptr_t> key;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;  // kernels inside the graph (for the launch counter)
+    int state = 0;          // 0 seen once (ran plain), 1 captured, -1 never capture
+};
+
 struct osbf_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -80,6 +90,13 @@ struct osbf_ctx {
     osbf_gpu::LaunchCounter lc;
     int passes_per_launch = 1;  // fast mode temporal blocking: 1 or 2
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host entry points: copy overlap
+    cudaStream_t capture = nullptr;                      // CUDA-graph capture stream
+    std::vector<GraphEntry> graphs;                      // small LRU of replayable calls
+    void drop_graphs() {
+        for (auto& gph : graphs)
+            if (gph.exec) cudaGraphExecDestroy(gph.exec);
+        graphs.clear();
+    }
 };
 
 namespace {
@@ -261,6 +278,71 @@ osbf_status jacobi(osbf_ctx* ctx, const osbf_gpu::PlaneView& input, const osbf_g
     return OSBF_OK;
 }
 
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("OSBF_GPU_GRAPHS");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// A multi-pass call is a fixed sequence of launches, so a repeated call
+// (same buffers, geometry, radius, passes) replays it as one CUDA graph:
+// the first call runs plainly (allocations, kernel attributes), the second
+// is captured on a private stream and instantiated, later ones are one
+// cudaGraphLaunch on the caller's stream.  Any change of argument or of a
+// scratch buffer is a different key.  OSBF_GPU_GRAPHS=0 disables it.
+template <typename Body>
+osbf_status run_graphed(osbf_ctx* ctx, std::vector<uintptr_t> key, cudaStream_t s, Body&& body) {
+    if (!graphs_enabled()) return body(s);
+    for (void* p : {ctx->ping.ptr, ctx->pong.ptr, ctx->rowpfx.ptr, ctx->sat.ptr})
+        key.push_back(reinterpret_cast<uintptr_t>(p));
+    for (size_t b : {ctx->ping.bytes, ctx->pong.bytes, ctx->rowpfx.bytes, ctx->sat.bytes})
+        key.push_back(b);
+    auto it = std::find_if(ctx->graphs.begin(), ctx->graphs.end(),
+                           [&](const GraphEntry& e) { return e.key == key; });
+    if (it == ctx->graphs.end()) {
+        if (ctx->graphs.size() >= 8) {  // evict the oldest
+            if (ctx->graphs.front().exec) cudaGraphExecDestroy(ctx->graphs.front().exec);
+            ctx->graphs.erase(ctx->graphs.begin());
+        }
+        GraphEntry e;
+        e.key = std::move(key);
+        ctx->graphs.push_back(std::move(e));
+        return body(s);  // first time: plain (may allocate; the key is re-taken next time)
+    }
+    if (it->state == -1) return body(s);
+    if (it->state == 0) {
+        if (!ctx->capture)
+            OSBF_CUDA(cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking), "stream");
+        const uint64_t before = ctx->lc.launches;
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal);
+        osbf_status st = OSBF_OK;
+        if (e == cudaSuccess) {
+            st = body(ctx->capture);
+            e = cudaStreamEndCapture(ctx->capture, &graph);
+        }
+        const uint64_t captured = ctx->lc.launches - before;  // kernels inside the graph
+        ctx->lc.launches = before;
+        cudaGraphExec_t exec = nullptr;
+        if (e == cudaSuccess && st == OSBF_OK && graph)
+            e = cudaGraphInstantiate(&exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e != cudaSuccess || st != OSBF_OK || !exec) {
+            cudaGetLastError();  // capture unsupported here: run plainly from now on
+            it->state = -1;
+            return body(s);
+        }
+        it->exec = exec;
+        it->launches = captured;
+        it->state = 1;
+    }
+    OSBF_CUDA(cudaGraphLaunch(it->exec, s), "graph launch");
+    ctx->lc.launches += it->launches;
+    return OSBF_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -298,6 +380,8 @@ osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx) {
     ctx->sat.release();
     ctx->host_in.release();
     ctx->host_out.release();
+    ctx->drop_graphs();
+    if (ctx->capture) cudaStreamDestroy(ctx->capture);
     if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
     if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
     cudaStreamDestroy(ctx->stream);
@@ -309,6 +393,8 @@ osbf_status osbf_gpu_ctx_trim(osbf_ctx* ctx) {
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
     cudaSetDevice(ctx->device);
     OSBF_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    OSBF_CUDA(cudaDeviceSynchronize(), "sync");  // graphs may run on caller streams
+    ctx->drop_graphs();
     ctx->ping.release();
     ctx->pong.release();
     ctx->rowpfx.release();
@@ -361,23 +447,34 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
     // Fast mode runs two passes per launch (temporal blocking) when enabled
     // and the radius has a two-pass kernel; otherwise one pass per launch.
     const bool tb2 = mode == OSBF_MODE_FAST && (ctx->passes_per_launch == 2 || tb2_env());
-    return jacobi(
-        ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, s,
-        [&](int remaining) { return tb2 && remaining >= 2 ? 2 : 1; },
-        [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int n,
-            bool* retry) -> osbf_status {
-            if (n == 2) {
-                const cudaError_t e = osbf_gpu::fast_step2(src, g, radius, dst, dp, dpl, s, ctx->lc);
-                if (e == cudaErrorNotSupported) {
-                    cudaGetLastError();
-                    *retry = true;
+    auto body = [&](cudaStream_t st_) {
+        return jacobi(
+            ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, st_,
+            [&](int remaining) { return tb2 && remaining >= 2 ? 2 : 1; },
+            [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int n,
+                bool* retry) -> osbf_status {
+                if (n == 2) {
+                    const cudaError_t e =
+                        osbf_gpu::fast_step2(src, g, radius, dst, dp, dpl, st_, ctx->lc);
+                    if (e == cudaErrorNotSupported) {
+                        cudaGetLastError();
+                        *retry = true;
+                        return OSBF_OK;
+                    }
+                    OSBF_CUDA(e, "fast two-pass step");
                     return OSBF_OK;
                 }
-                OSBF_CUDA(e, "fast two-pass step");
-                return OSBF_OK;
-            }
-            return one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, s);
-        });
+                return one_pass(ctx, src, g, radius, dst, dp, dpl, nullptr, nullptr, mode, st_);
+            });
+    };
+    const std::vector<uintptr_t> key = {
+        1, static_cast<uintptr_t>(in_dtype), reinterpret_cast<uintptr_t>(d_in), in_pitch,
+        in_plane_stride, reinterpret_cast<uintptr_t>(d_out), out_pitch, out_plane_stride,
+        static_cast<uintptr_t>(width), static_cast<uintptr_t>(height),
+        static_cast<uintptr_t>(batch), static_cast<uintptr_t>(radius),
+        static_cast<uintptr_t>(iterations), static_cast<uintptr_t>(mode),
+        static_cast<uintptr_t>(tb2)};
+    return run_graphed(ctx, key, s, body);
 }
 
 osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
@@ -410,15 +507,26 @@ osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
     const size_t ns = static_cast<size_t>(batch) * (width + 1) * (height + 1);
     OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");
     OSBF_CUDA(ctx->sat.ensure(ns * sizeof(double)), "alloc sat");
-    return jacobi(
-        ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, s, [](int) { return 1; },
-        [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int,
-            bool*) -> osbf_status {
-            OSBF_CUDA(osbf_gpu::fastosbf_pass(src, g, radius, ctx->rowpfx.as<double>(),
-                                              ctx->sat.as<double>(), dst, dp, dpl, s, ctx->lc),
-                      "fast_osbf pass");
-            return OSBF_OK;
-        });
+    auto body = [&](cudaStream_t st_) {
+        return jacobi(
+            ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, st_,
+            [](int) { return 1; },
+            [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int,
+                bool*) -> osbf_status {
+                OSBF_CUDA(osbf_gpu::fastosbf_pass(src, g, radius, ctx->rowpfx.as<double>(),
+                                                  ctx->sat.as<double>(), dst, dp, dpl, st_,
+                                                  ctx->lc),
+                          "fast_osbf pass");
+                return OSBF_OK;
+            });
+    };
+    const std::vector<uintptr_t> key = {
+        2, static_cast<uintptr_t>(in_dtype), reinterpret_cast<uintptr_t>(d_in), in_pitch,
+        in_plane_stride, reinterpret_cast<uintptr_t>(d_out), out_pitch, out_plane_stride,
+        static_cast<uintptr_t>(width), static_cast<uintptr_t>(height),
+        static_cast<uintptr_t>(batch), static_cast<uintptr_t>(radius),
+        static_cast<uintptr_t>(iterations)};
+    return run_graphed(ctx, key, s, body);
 }
 
 osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,

@@ -84,3 +84,32 @@ def test_host_batch_pipeline_matches_device_path(ctx, mode, r):
     got = ctx.osbf_host(x, r, 2, mode=mode)
     want = ctx.iterate(torch.from_numpy(x).cuda(), r, 2, mode=mode).cpu().numpy()
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_repeated_calls_replay_a_graph(ctx, oracle_lib, mode):
+    """A repeated call with the same buffers is replayed as one CUDA graph
+    (captured on the second call): results follow the CURRENT input contents,
+    and the launch counter still counts the kernels inside the graph."""
+    import torch
+
+    x = torch.rand((3, 96, 80), dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    before = ctx.launches
+    ctx.iterate(x, 2, 4, mode=mode, out=y)
+    per_call = ctx.launches - before
+    for _ in range(3):  # plain, capture, replay, replay
+        ctx.iterate(x, 2, 4, mode=mode, out=y)
+    assert ctx.launches - before == 4 * per_call
+    x.copy_(torch.rand_like(x) * 255)  # new contents, same buffers -> replay
+    ctx.iterate(x, 2, 4, mode=mode, out=y)
+    got = y.cpu().numpy()
+    for b in range(3):
+        want = oracle_lib.osbf(x[b].cpu().numpy(), 2, 4)
+        if mode == "exact":
+            assert np.array_equal(bits(got[b]), bits(want))
+        else:
+            assert np.abs(got[b] - want).max() <= 1e-9 * 255
+    z = torch.empty_like(x)  # a different output buffer is a different graph key
+    ctx.iterate(x, 2, 4, mode=mode, out=z)
+    assert torch.equal(z, y)
