@@ -59,7 +59,8 @@ typedef enum osbf_mode {
     /* Tile-local fp64 sums (no whole-image prefix, no drift on huge images),
      * same selection rule.  Bit-identical to the reference whenever the
      * window sums are exact (integer-valued input, e.g. uint8 first pass);
-     * otherwise within a few fp64 ulps per pass. */
+     * otherwise within a few fp64 ulps per pass.  Radii above 16 run the
+     * exact kernels. */
     OSBF_MODE_FAST = 1
 } osbf_mode;
 

@@ -156,6 +156,10 @@ bool tb2_env() {
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
                      int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
                      osbf_mode mode, cudaStream_t s) {
+    // Fast mode has compiled kernels up to kFastMaxRadius; larger windows run
+    // the exact GPU kernels (bit-identical to the reference, hence also
+    // within the fast mode's tolerance), like the reference accepts any r.
+    if (mode == OSBF_MODE_FAST && r > osbf_gpu::kFastMaxRadius) mode = OSBF_MODE_EXACT;
     if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius) {
         // fused exact path: row carries + strip kernel (same bits as below)
         OSBF_CUDA(ctx->rowpfx.ensure(osbf_gpu::exact_fused_carry_elems(g) * sizeof(double)),
@@ -175,10 +179,6 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
                                          s, ctx->lc),
                   "exact select");
     } else {
-        if (r > osbf_gpu::kFastMaxRadius)
-            return fail(OSBF_ERR_INVALID_ARGUMENT,
-                        "fast mode supports radius <= %d (got %d); use OSBF_MODE_EXACT",
-                        osbf_gpu::kFastMaxRadius, r);
         OSBF_CUDA(osbf_gpu::fast_step(src, g, r, dst, dp, dpl, means, sel, s, ctx->lc),
                   "fast step");
     }

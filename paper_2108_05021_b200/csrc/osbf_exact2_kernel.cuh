@@ -90,8 +90,12 @@ struct XLay {
     // k's last barrier.  The stencil strips use 3; the carries pass (no
     // stencil, short iterations) stages deeper to cover DRAM latency.
     static constexpr int NUB = NUBV;
+    // staged-carry buffers: blocks k+1 .. k+NUB-1 can be in flight, i.e.
+    // NUB-1 of them (2 for the stencil strips, which keeps r=8 at two CTAs
+    // per SM)
+    static constexpr int NCS = NUB - 1;
     static constexpr size_t SMEM = sizeof(double) * (NUB * static_cast<size_t>(U_ELEMS) + BR * PR +
-                                                     NRING * NCC + NUB * BR * NSEGR);
+                                                     NRING * NCC + NCS * BR * NSEGR);
     // warps: column chains on [0, CCW), the early stencil rows on the rest;
     // row prefixes on [0, RRW), the late stencil rows on the rest
     static constexpr int CCW = (NCC + 31) / 32;
@@ -301,9 +305,17 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
             // With every |a_i - u| finite, "first i with the smallest d_i"
             // (strict <, filters2d.hpp:78) is what a stable depth-3 tournament
             // returns; non-finite pixels (NaN/inf input) keep the sequential
-            // rule, under which such windows are never selected.
-            const double dsum = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
-            if (fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL)) {
+            // rule, under which such windows are never selected.  SAFE strips
+            // have only finite, in-range table values (a non-finite sample u
+            // would have made its table column non-finite), so every d_i is
+            // finite there without checking.
+            bool finite = SAFE;
+            if (!SAFE) {
+                const double dsum =
+                    ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
+                finite = fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL);
+            }
+            if (finite) {
                 auto pick = [](double& d0, double& a0, double d1, double a1) {
                     const bool t = d1 < d0;
                     d0 = t ? d1 : d0;
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(NT, 2)
     double* Ubuf = sm;                          // NUB x [BR][PUB]
     double* Rb = sm + L::NUB * L::U_ELEMS;      // [BR][PR]:  Rb[rr][j] = R(X0-R-1+j, y0+rr)
     double* Cr = Rb + BR * L::PR;               // [NRING][NCC]: table rows, column cx = X0-R+t
-    double* cs = Cr + L::NRING * L::NCC;        // NUB x [NSEGR][BR] staged carries
+    double* cs = Cr + L::NRING * L::NCC;        // NCS x [NSEGR][BR] staged carries
     const int b = blockIdx.y;
     const int X0 = blockIdx.x * TW;
     const int xs_raw = X0 - R;
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(NT, 2)
     const bool aligned16 = sizeof(T) == 8 && (pitch % 2 == 0) &&
                            (reinterpret_cast<uintptr_t>(src) % 16 == 0);
     auto U_of = [&](int k) { return Ubuf + (k % L::NUB) * L::U_ELEMS; };
-    auto cs_of = [&](int k) { return cs + (k % L::NUB) * BR * L::NSEGR; };
+    auto cs_of = [&](int k) { return cs + (k % L::NCS) * BR * L::NSEGR; };
     auto stage = [&](int k) {  // block k, or an empty group past the end
         if (k < nblocks)
             stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + k * BR, W, H,

@@ -113,3 +113,13 @@ def test_repeated_calls_replay_a_graph(ctx, oracle_lib, mode):
     z = torch.empty_like(x)  # a different output buffer is a different graph key
     ctx.iterate(x, 2, 4, mode=mode, out=z)
     assert torch.equal(z, y)
+
+
+def test_fast_mode_large_radius_runs_exact_kernels(ctx, oracle_lib):
+    """The reference accepts any r; fast mode has kernels up to r=16 and runs
+    larger windows on the exact kernels (bit-identical)."""
+    import torch
+
+    p = np.random.default_rng(3).random((90, 70)) * 255
+    got = ctx.iterate(torch.from_numpy(p).cuda(), 23, 2, mode="fast").cpu().numpy()
+    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 23, 2)))
