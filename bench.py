@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--radius", type=int, default=None)
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--c5-scaling", choices=("strong", "weak"), default="strong",
+                    help="C5: fixed 32768^2 image over N GPUs (strong) or a 32768 x 4096 "
+                         "band per GPU, 32768 x 4096N in total (weak, SURVEY §8e)")
     ap.add_argument("--exchange", choices=("push", "nccl"), default="push",
                     help="C5 halo exchange: fused into the pass kernel (symmetric memory) "
                          "or NCCL send/recv after it")
@@ -277,8 +280,8 @@ def run_reference(args, world, rank):
 
 
 def run_c5(args, world, rank, local):
-    """C5: one 32768^2 float32 image, row bands across ranks (strong scaling),
-    fast mode, per-pass halo exchange between neighbours (fused into the pass
+    """C5: one 32768^2 float32 image, row bands across ranks (strong scaling;
+    --c5-scaling weak: a 32768 x 4096 band per rank), fast mode, per-pass halo exchange between neighbours (fused into the pass
     kernel through symmetric memory, or NCCL send/recv with --exchange nccl)."""
     import torch
 
@@ -289,7 +292,8 @@ def run_c5(args, world, rank, local):
     cfg = synth.CONFIGS["C5"]
     r = args.radius or cfg.radius
     iters = args.iterations or cfg.iterations
-    H = W = 32768
+    W = 32768
+    H = 4096 * world if args.c5_scaling == "weak" else 32768
     x = synth.make_c5_on_device(H, W, seed=5)  # identical on every rank (Philox)
     lay = BandLayout.make(H, W, r, world, rank)
     band = x[lay.row0:lay.row1]
@@ -324,8 +328,10 @@ def run_c5(args, world, rank, local):
         "metric": METRIC, "value": round(value, 3), "unit": "Mpx-iter/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, r, iters), "height": H, "width": W,
+        "scaling": args.c5_scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, r, iters) + (
+                       f" (weak: {W} x {H} = 4096 rows per GPU)" if args.c5_scaling == "weak"
+                       else ""), "height": H, "width": W,
                    "radius": r, "iterations": iters, "mode": "fast",
                    "parallelism": f"row bands x{world}, {r}-row halo exchange per pass "
                                   + ("(fused: pass kernel stores into the neighbours' "
