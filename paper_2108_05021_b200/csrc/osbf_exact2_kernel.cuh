@@ -65,12 +65,15 @@ namespace ex2 {
 
 constexpr int TW = 32;   // output columns per strip
 constexpr int SW = 16;   // spacing of the stored row carries (columns)
-constexpr int BR = 32;   // rows per block
+constexpr int BR = 32;   // rows per block (radii <= 8; larger radii use 16, see XLay)
 constexpr int NT = 256;  // threads per strip CTA
 constexpr int NTK1 = 64; // threads per carry CTA (2 warps, 32 rows each)
 
 template <int R, int NUBV = 3>
 struct XLay {
+    // rows per block: 16 above r=8 halves the U / row-sum / ring footprint
+    // (r=16: 149 KB -> 74 KB, one CTA per SM -> three)
+    static constexpr int BR = R > 8 ? 16 : ex2::BR;
     // staged U columns: [xs, xs + NU) with xs = floor((X0-R)/SW)*SW >= X0-R-SW+1,
     // covering up to X0 + TW + R - 1
     static constexpr int NU = TW + 2 * R + SW;
@@ -80,7 +83,7 @@ struct XLay {
     static constexpr int NCC = TW + 2 * R + 1;  // table columns cx in [X0-R, X0+TW+R]
     static constexpr int PR = NCC | 1;
     // table rows kept: [y0-BR-R, y0+BR] (2BR+R+1 rows), as a power of two
-    static constexpr int NRING = (2 * BR + R + 2) <= 128 ? 128 : 256;
+    static constexpr int NRING = (2 * BR + R + 2) <= 64 ? 64 : ((2 * BR + R + 2) <= 128 ? 128 : 256);
     static constexpr int U_ELEMS = BR * PUB;
     // row segments of SW columns between stored carries (RR parallelism)
     static constexpr int NSEGR = (NU + SW - 1) / SW;
@@ -203,6 +206,7 @@ __device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pi
                                             double* __restrict__ U, double* __restrict__ cs,
                                             bool aligned16) {
     using L = XLay<R>;
+    constexpr int BR = L::BR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if constexpr (sizeof(T) == 8) {
         // warp per row, 16-byte copies (xs is a multiple of SW = 16 columns)
@@ -375,6 +379,7 @@ __global__ void __launch_bounds__(NT, 2)
                 size_t opitch, size_t oplane, int W, int H, int band_h,
                 double* __restrict__ ccar) {
     using L = XLay<R, CARRIES ? 6 : 3>;
+    constexpr int BR = L::BR;
     constexpr int AHEAD = L::NUB - 2;  // blocks staged ahead of the row prefixes
     extern __shared__ double sm[];
     double* Ubuf = sm;                          // NUB x [BR][PUB]
