@@ -164,13 +164,21 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
         const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
         cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
     }
-    // Whole chunk of interior outputs (the common case): no per-row branch,
-    // so the unrolled rows interleave.  Otherwise per-row checks.
+    const bool warp_interior = __all_sync(0xffffffffu, gx < W && !col_border);
+    const bool warp_border = !warp_interior;
+    // Chunk kinds (all warp-uniform, so no lane of a warp runs a different
+    // select than its neighbours):
+    //   0  every row an output row away from the image top/bottom, no border
+    //      column in the warp: interior reciprocals, no per-row branch;
+    //   1  same rows, but the warp holds border (or out-of-image) columns:
+    //      the clipped-count select for all its lanes (for a full window it
+    //      forms exactly the interior reciprocal, select_store);
+    //   2  otherwise: per-row output / border checks.
     // u / uprev: this column's samples in the chunk's / previous chunk's slot
     // (the centre sample of row k sits R rows up).
-    auto chunk_rows = [&](auto interior, const double* h, const T* u, const T* uprev, int iy0,
+    auto chunk_rows = [&](auto kind_tag, const double* h, const T* u, const T* uprev, int iy0,
                           const ColFactors& cf) {
-        constexpr bool IN = decltype(interior)::value;
+        constexpr int KIND = decltype(kind_tag)::value;
 #pragma unroll
         for (int k = 0; k < L; ++k) {
             const double a = h[k * Ly::HWP], c = h[k * Ly::HWP + R];
@@ -186,22 +194,25 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
             q2[k] = P2;
             qg[k] = PG;
             const int iy = iy0 + k;  // output row Y0 + iy - R when iy in [R, R + nout)
-            if (IN || (iy >= R && iy < R + nout && gx < W)) {
+            if (KIND < 2 || (iy >= R && iy < R + nout)) {
                 const int gy = Y0 + iy - R;
                 const double uc = to_f64(k >= R ? u[(k - R) * Ly::BW] : uprev[(k - R + CH) * Ly::BW]);
                 const double S[8] = {P1 - p1m, P2 - p2m, p2y - p2o, p1y - p1o,
                                      P1 - p1o, P2 - p2o, PG - pgm,  pgy - pgo};
                 double* o = ocol + static_cast<size_t>(gy - band.y_out0) * out_pitch;
-                if (IN || !(col_border || gy < R || gy >= Himg - R))
-                    select_store<R, EXACT_DIV, false, false>(S, uc, gx, gy, W, Himg, b, o,
-                                                             nullptr, nullptr, cf, rtab);
-                else
+                const bool clipped = KIND == 1 || (KIND == 2 && (warp_border || gy < R ||
+                                                                 gy >= Himg - R));
+                if (KIND == 0 || (KIND == 2 && !clipped)) {
+                    if (KIND == 0 || gx < W)
+                        select_store<R, EXACT_DIV, false, false>(S, uc, gx, gy, W, Himg, b, o,
+                                                                 nullptr, nullptr, cf, rtab);
+                } else if (gx < W) {
                     select_store<R, EXACT_DIV, true, false>(S, uc, gx, gy, W, Himg, b, o, nullptr,
                                                             nullptr, cf, rtab);
+                }
             }
         }
     };
-    const bool warp_interior = __all_sync(0xffffffffu, gx < W && !col_border);
     for (int c = 0; c < nchunks; ++c) {
         const int q = c % Ly::NU, qp = (c + Ly::NU - 1) % Ly::NU;
         tma::mbar_wait(&ufull[q], (c / Ly::NU) & 1);
@@ -211,10 +222,13 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
         const double* h = Hw + lane;
         const int iy0 = c * CH - R;  // strip row index (input coords) of the k = 0 output
         const int gy0 = Y0 + iy0 - R;
-        if (warp_interior && iy0 >= R && iy0 + L <= R + nout && gy0 >= R && gy0 + L <= Himg - R)
-            chunk_rows(std::true_type{}, h, u, uprev, iy0, cf);
+        const bool rows_full = iy0 >= R && iy0 + L <= R + nout && gy0 >= R && gy0 + L <= Himg - R;
+        if (rows_full && warp_interior)
+            chunk_rows(std::integral_constant<int, 0>{}, h, u, uprev, iy0, cf);
+        else if (rows_full)
+            chunk_rows(std::integral_constant<int, 1>{}, h, u, uprev, iy0, cf);
         else
-            chunk_rows(std::false_type{}, h, u, uprev, iy0, cf);
+            chunk_rows(std::integral_constant<int, 2>{}, h, u, uprev, iy0, cf);
         __syncwarp();  // slice and slot reads done before reuse
         // the previous chunk's slot (centre samples) is free now
         if (lane == 0 && c > 0) tma::mbar_arrive(&uempty[qp]);
