@@ -33,7 +33,7 @@ namespace osbf_gpu {
 namespace fastk {
 
 constexpr int kStreamMinRadius = 5;
-constexpr int kStreamMaxRadius = 7;
+constexpr int kStreamMaxRadius = 9;
 
 template <int R, typename T>
 struct SLay {
