@@ -33,13 +33,13 @@ namespace osbf_gpu {
 namespace fastk {
 
 constexpr int kStreamMinRadius = 5;
-constexpr int kStreamMaxRadius = 9;
+constexpr int kStreamMaxRadius = 10;
 
 template <int R, typename T>
 struct SLay {
     static constexpr int NWB = 4;               // column warps (one per SM sub-partition)
     static constexpr int TWS = 32 * NWB;        // output columns per strip
-    static constexpr int NTS = 32 * (NWB + 1);  // + 1 TMA producer warp
+    static constexpr int NTS = 32 * NWB;        // thread 0 also issues the TMA loads
     static constexpr int L = 2 * R + 2;         // register ring length
     static constexpr int CH = L;                // rows per chunk (ring index = row in chunk)
     static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
@@ -62,8 +62,11 @@ struct SLay {
     static constexpr size_t PAD = 512;  // equal-length arm segments may read past the last row
     static constexpr size_t kSmemMax = 227 * 1024;
     // U ring depth: as deep as MINB CTAs per SM allow (3..8 slots)
-    static constexpr int MINB = R <= 5 ? 3 : 2;  // CTAs per SM (register budget)
-    static constexpr size_t kCtaSmem = (MINB == 3 ? 74 : 112) * 1024;
+    // CTAs per SM in the launch bound: 4-warp CTAs put MINB warps on each SM
+    // sub-partition, whose 64K-register file then caps a thread at 128 / 168
+    // / 255 registers (the prefix rings need 6R+6 doubles)
+    static constexpr int MINB = R <= 5 ? 4 : (R <= 7 ? 3 : 2);
+    static constexpr size_t kCtaSmem = (MINB == 4 ? 56 : MINB == 3 ? 74 : 112) * 1024;
     static constexpr int NU_FIT = static_cast<int>((kCtaSmem - 128 - PAD - H_BYTES) / U_BYTES);
     static constexpr int NU = NU_FIT > 8 ? 8 : (NU_FIT < 3 ? 3 : NU_FIT);
     static constexpr size_t SMEM = 128 + NU * U_BYTES + PAD + H_BYTES;
@@ -93,11 +96,11 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
     using Ly = SLay<R, T>;
     constexpr int L = Ly::L, CH = Ly::CH;
     extern __shared__ unsigned char smem_raw[];
-    // ufull: TMA landed (1 arrive + tx); uempty: slot consumed by every
-    // column warp.  Each column warp computes the arms of its own 32 + R
-    // columns (private slice, no cross-warp dependency) and then its rows;
-    // no CTA-wide barrier after the prologue.
-    __shared__ uint64_t ufull[Ly::NU], uempty[Ly::NU];
+    // ufull: TMA landed (1 arrive + tx).  Each column warp computes the arms
+    // of its own 32 + R columns (private slice, no cross-warp dependency) and
+    // then its rows; one barrier per chunk frees the previous chunk's slot,
+    // which thread 0 refills with TMA.
+    __shared__ uint64_t ufull[Ly::NU];
     __shared__ double rtab[2 * R + 2];
     const uint32_t base = tma::smem_u32(smem_raw);
     unsigned char* sm = smem_raw + ((128u - (base & 127u)) & 127u);
@@ -112,30 +115,19 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
     const int nchunks = (nout + 2 * R + CH - 1) / CH;
     const int b = blockIdx.z;
     const int ytma0 = Y0 - R - band.y_in0;  // input-buffer row of strip input row 0
-    constexpr int PRODUCER = Ly::NWB;
 
     if (tid < 2 * R + 2) rtab[tid] = tid ? 1.0 / tid : 0.0;
     if (tid == 0) {
-        for (int q = 0; q < Ly::NU; ++q) {
-            tma::mbar_init(&ufull[q], 1);
-            tma::mbar_init(&uempty[q], Ly::NWB);
-        }
+        for (int q = 0; q < Ly::NU; ++q) tma::mbar_init(&ufull[q], 1);
     }
     __syncthreads();
-
-    if (warp == PRODUCER) {
-        if (lane == 0) {
-            for (int c = 0; c < nchunks; ++c) {
-                const int q = c % Ly::NU;
-                // slot of chunk c - NU: released once chunk c - NU + 1 is done
-                if (c >= Ly::NU) tma::mbar_wait(&uempty[q], ((c / Ly::NU) - 1) & 1);
-                tma::mbar_arrive_expect_tx(&ufull[q], Ly::CHUNK_BYTES);
-                tma::load_3d(Ub + q * Ly::U_ELEMS, &tmap, X0 - Ly::RA, ytma0 + c * CH, b,
-                             &ufull[q]);
-            }
-        }
-        return;
-    }
+    auto issue = [&](int c) {  // chunk c into slot c % NU (thread 0)
+        const int q = c % Ly::NU;
+        tma::mbar_arrive_expect_tx(&ufull[q], Ly::CHUNK_BYTES);
+        tma::load_3d(Ub + q * Ly::U_ELEMS, &tmap, X0 - Ly::RA, ytma0 + c * CH, b, &ufull[q]);
+    };
+    if (tid == 0)
+        for (int c = 0; c < Ly::NU && c < nchunks; ++c) issue(c);
 
     // Arms of this warp's slice for the chunk in U: lanes = 16 rows x 2 segments.
     auto arms = [&](const T* U) {
@@ -229,9 +221,14 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
             chunk_rows(std::integral_constant<int, 1>{}, h, u, uprev, iy0, cf);
         else
             chunk_rows(std::integral_constant<int, 2>{}, h, u, uprev, iy0, cf);
-        __syncwarp();  // slice and slot reads done before reuse
-        // the previous chunk's slot (centre samples) is free now
-        if (lane == 0 && c > 0) tma::mbar_arrive(&uempty[qp]);
+        __syncwarp();  // slice reads done before the next chunk's arms
+        // every warp is done with chunk c, so the previous chunk's slot (its
+        // centre samples were the last readers) takes chunk c - 1 + NU
+        __syncthreads();
+        if (tid == 0 && c > 0 && c - 1 + Ly::NU < nchunks) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(c - 1 + Ly::NU);
+        }
     }
     if (gx < W)
         push_tail(band, out + static_cast<size_t>(b) * out_plane, out_pitch, gx, Y0, Y0 + nout);
