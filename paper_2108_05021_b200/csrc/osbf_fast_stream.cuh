@@ -5,7 +5,7 @@
 // output rows, and walks down it once:
 //
 //   * A producer warp streams the strip (plus an R-column halo each side)
-//     with TMA in chunks of CH = 2R+2 rows through a 3-4 slot ring
+//     with TMA in chunks of CH = 2R+2 (R+1 above r=10) rows through a 3-8 slot ring
 //     (mbarrier full/empty pairs; hardware zero fill outside the image, so
 //     clipped windows need no special casing; the valid counts are the
 //     reference's clipped ones, integral.hpp:53-61).
@@ -33,7 +33,7 @@ namespace osbf_gpu {
 namespace fastk {
 
 constexpr int kStreamMinRadius = 5;
-constexpr int kStreamMaxRadius = 10;
+constexpr int kStreamMaxRadius = 16;
 
 template <int R, typename T>
 struct SLay {
@@ -41,7 +41,11 @@ struct SLay {
     static constexpr int TWS = 32 * NWB;        // output columns per strip
     static constexpr int NTS = 32 * NWB;        // thread 0 also issues the TMA loads
     static constexpr int L = 2 * R + 2;         // register ring length
-    static constexpr int CH = L;                // rows per chunk (ring index = row in chunk)
+    // rows per chunk: the ring length, or half of it above r=10 (halves the
+    // shared-memory slots so two CTAs still fit; chunks then alternate
+    // between the two halves of the ring, a compile-time parity)
+    static constexpr int NPAR = R > 10 ? 2 : 1;
+    static constexpr int CH = L / NPAR;
     static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
     static constexpr int RA = (R + ALIGN - 1) / ALIGN * ALIGN;  // TMA x start: X0 - RA
     static constexpr int XOFF = RA - R;
@@ -168,23 +172,25 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
     //   2  otherwise: per-row output / border checks.
     // u / uprev: this column's samples in the chunk's / previous chunk's slot
     // (the centre sample of row k sits R rows up).
-    auto chunk_rows = [&](auto kind_tag, const double* h, const T* u, const T* uprev, int iy0,
-                          const ColFactors& cf) {
+    auto chunk_rows = [&](auto kind_tag, auto parity_tag, const double* h, const T* u,
+                          const T* uprev, int iy0, const ColFactors& cf) {
         constexpr int KIND = decltype(kind_tag)::value;
+        constexpr int RB = decltype(parity_tag)::value * CH;  // ring slot of row 0
 #pragma unroll
-        for (int k = 0; k < L; ++k) {
+        for (int k = 0; k < CH; ++k) {
             const double a = h[k * Ly::HWP], c = h[k * Ly::HWP + R];
             const double e = to_f64(u[k * Ly::BW]);
             P1 += a;
             P2 += c;
             PG += (a + c) - e;
-            const int iY = (k + R + 2) % L, iYm1 = (k + R + 1) % L, iOld = (k + 1) % L;
+            const int iY = (RB + k + R + 2) % L, iYm1 = (RB + k + R + 1) % L,
+                      iOld = (RB + k + 1) % L;
             const double p1y = q1[iY], p1m = q1[iYm1], p1o = q1[iOld];
             const double p2y = q2[iY], p2m = q2[iYm1], p2o = q2[iOld];
             const double pgy = qg[iY], pgm = qg[iYm1], pgo = qg[iOld];
-            q1[k] = P1;
-            q2[k] = P2;
-            qg[k] = PG;
+            q1[RB + k] = P1;
+            q2[RB + k] = P2;
+            qg[RB + k] = PG;
             const int iy = iy0 + k;  // output row Y0 + iy - R when iy in [R, R + nout)
             if (KIND < 2 || (iy >= R && iy < R + nout)) {
                 const int gy = Y0 + iy - R;
@@ -214,13 +220,20 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
         const double* h = Hw + lane;
         const int iy0 = c * CH - R;  // strip row index (input coords) of the k = 0 output
         const int gy0 = Y0 + iy0 - R;
-        const bool rows_full = iy0 >= R && iy0 + L <= R + nout && gy0 >= R && gy0 + L <= Himg - R;
-        if (rows_full && warp_interior)
-            chunk_rows(std::integral_constant<int, 0>{}, h, u, uprev, iy0, cf);
-        else if (rows_full)
-            chunk_rows(std::integral_constant<int, 1>{}, h, u, uprev, iy0, cf);
+        const bool rows_full =
+            iy0 >= R && iy0 + CH <= R + nout && gy0 >= R && gy0 + CH <= Himg - R;
+        auto run = [&](auto parity) {
+            if (rows_full && warp_interior)
+                chunk_rows(std::integral_constant<int, 0>{}, parity, h, u, uprev, iy0, cf);
+            else if (rows_full)
+                chunk_rows(std::integral_constant<int, 1>{}, parity, h, u, uprev, iy0, cf);
+            else
+                chunk_rows(std::integral_constant<int, 2>{}, parity, h, u, uprev, iy0, cf);
+        };
+        if (Ly::NPAR == 2 && (c & 1))
+            run(std::integral_constant<int, Ly::NPAR - 1>{});
         else
-            chunk_rows(std::integral_constant<int, 2>{}, h, u, uprev, iy0, cf);
+            run(std::integral_constant<int, 0>{});
         __syncwarp();  // slice reads done before the next chunk's arms
         // every warp is done with chunk c, so the previous chunk's slot (its
         // centre samples were the last readers) takes chunk c - 1 + NU

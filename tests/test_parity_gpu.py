@@ -205,7 +205,7 @@ def test_in_place_and_pitched(ctx, oracle_lib):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
 
 
-STREAM_RADII = range(5, 11)  # fast radii served by the streaming column-strip kernel
+STREAM_RADII = range(5, 17)  # fast radii served by the streaming column-strip kernel
 
 
 @pytest.mark.parametrize("r", [2, 7, 12])
