@@ -93,6 +93,27 @@ def test_exact_row_bands_bit_exact(ctx, oracle_lib, shape, r, scale):
     assert np.array_equal(bits(got), bits(want))
 
 
+@pytest.mark.parametrize("r", range(1, 17))
+def test_fast_every_radius_random_shapes(ctx, oracle_lib, r):
+    """Fast mode at every compiled radius (tile, streaming and half-chunk
+    streaming kernels) on ragged shapes — narrower / shorter than a window,
+    a strip, a chunk or a band, and a batch — within the float tolerance of
+    the reference; uint8 first pass bit-exact."""
+    import torch
+
+    rng = np.random.default_rng(900 + r)
+    shapes = [(1, 3, 2), (1, r, 2 * r + 1), (2, 37, 300), (1, 700, 129), (3, 130, 257)]
+    for shape in shapes:
+        p = rng.random(shape) * 255.0
+        got = ctx.iterate(torch.from_numpy(p).cuda(), r, 3, mode="fast").cpu().numpy()
+        want = np.stack([oracle_lib.osbf(c, r, 3) for c in p])
+        assert float(np.abs(got - want).max()) <= FLOAT_TOL * 255.0, shape
+    u8 = rng.integers(0, 256, (2, 300, 290), dtype=np.uint8)
+    got = ctx.iterate(torch.from_numpy(u8).cuda(), r, 1, mode="fast").cpu().numpy()
+    want = np.stack([oracle_lib.osbf(c.astype(np.float64), r, 1) for c in u8])
+    assert np.array_equal(bits(got), bits(want))
+
+
 def test_exact_sat_bit_exact(ctx, oracle_lib):
     rng = np.random.default_rng(7)
     for h, w in [(1, 1), (3, 200), (257, 65), (300, 301)]:
