@@ -1,8 +1,17 @@
-// Fast-mode kernel templates (see osbf_fast.cu for the design notes).
+// Fast-mode kernel templates.
 #pragma once
-// Fast mode: one OSBF pass with tile-local fp64 box sums.
+// Fast mode: one OSBF pass with local fp64 box sums (no whole-image prefix).
+// Which kernel runs (launch_dtype below):
+//   r <= 4      fast_tma_step     one TMA-staged tile per CTA, each column
+//                                 thread forms its arms from 2r+1 loads
+//   5 <= r <= 16  fast_stream_step  column strips streamed through a TMA ring
+//                                 with register prefix rings
+//                                 (osbf_fast_stream.cuh)
+//   otherwise   fast_sep_step     the two-phase tile kernel described here:
+//                                 layouts TMA cannot describe, and the
+//                                 per-pixel diagnostics (means / selection)
 //
-// Each CTA owns a TW x TH output tile.  It stages the tile plus an R-pixel
+// fast_sep_step: each CTA owns a TW x TH output tile.  It stages the tile plus an R-pixel
 // halo in shared memory (zero outside the image, so clipped window sums need
 // no special casing; only the valid counts do, integral.hpp:53-61) and
 // evaluates the eight one-sided windows of the reference (core.hpp:212-225)
