@@ -209,18 +209,11 @@ static_assert(kExactFusedMaxRadius == 16, "update kExact2");
 template <typename T>
 cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carries, int nsc,
                            cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(ex2::exact_row_carries<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(ex2::K1_SMEM));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(ex2::K1D_SMEM));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> done_k1{0}, done_k1d{0};
+    cudaError_t e = ensure_smem(ex2::exact_row_carries<T>, ex2::K1_SMEM, done_k1);
+    if (e == cudaSuccess)
+        e = ensure_smem(ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>, ex2::K1D_SMEM, done_k1d);
+    if (e != cudaSuccess) return e;
     const long long rows = static_cast<long long>(g.batch) * g.height;
     const long long warps = (rows + 31) / 32;
     if (warps <= 2 * 148) {  // about one warp per SM: deep single-warp CTAs

@@ -536,18 +536,10 @@ cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double*
     const int nbands = band_h > 0 ? (g.height + band_h - 1) / band_h : 1;
     auto go = [&](auto tag) -> cudaError_t {
         using T = decltype(tag);
-        static bool configured = false;
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(ex2::exact_strip<R, T, false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(L::SMEM));
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(ex2::exact_strip<R, T, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(LC::SMEM));
-            if (e != cudaSuccess) return e;
-            configured = true;
-        }
+        static std::atomic<unsigned long long> done_s{0}, done_c{0};
+        cudaError_t e0 = ensure_smem(ex2::exact_strip<R, T, false>, L::SMEM, done_s);
+        if (e0 == cudaSuccess) e0 = ensure_smem(ex2::exact_strip<R, T, true>, LC::SMEM, done_c);
+        if (e0 != cudaSuccess) return e0;
         const T* base = static_cast<const T*>(in.base);
         if (nbands > 1) {
             ex2::exact_strip<R, T, true><<<dim3(strips, g.batch, 1), ex2::NT, LC::SMEM, s>>>(

@@ -425,14 +425,9 @@ template <int R, typename T, bool EXACT_DIV, bool DIAG>
 cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t op, size_t opl,
                      double* means, uint8_t* sel, cudaStream_t s) {
     constexpr size_t smem = Lay<R>::SMEM;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_sep_step<R, T, EXACT_DIV, DIAG>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fast_sep_step<R, T, EXACT_DIV, DIAG>, smem, done))
+        return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
     fast_sep_step<R, T, EXACT_DIV, DIAG><<<grid, NT, smem, s>>>(
         static_cast<const T*>(in.base), in.pitch, in.plane, out, op, opl, means, sel, g.width,
@@ -576,14 +571,8 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
     if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
         return cudaErrorNotSupported;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_tma_step<R, T, EXACT_DIV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Ly::SMEM));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fast_tma_step<R, T, EXACT_DIV>, Ly::SMEM, done)) return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
     fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                               band_of(g));
@@ -814,14 +803,8 @@ cudaError_t launch_tma2(const PlaneView& in, const Geometry& g, double* out, siz
     if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
         return cudaErrorNotSupported;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_tma_step2<R, T, EXACT1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Ly::SMEM));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fast_tma_step2<R, T, EXACT1>, Ly::SMEM, done)) return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
     fast_tma_step2<R, T, EXACT1><<<grid, Ly::NTT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                  band_of(g));

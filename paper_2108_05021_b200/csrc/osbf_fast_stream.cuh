@@ -266,14 +266,8 @@ cudaError_t launch_stream(const PlaneView& in, const Geometry& g, double* out, s
     if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::CH))
         return cudaErrorNotSupported;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fast_stream_step<R, T, EXACT_DIV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Ly::SMEM));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fast_stream_step<R, T, EXACT_DIV>, Ly::SMEM, done)) return e;
     // Strips walk in 512-row bands (each band re-reads a 2R-row halo): a
     // single plane still fills the SMs and a batch ends in a short last wave
     // (measured best of 128..2048 rows on 256 x 1024^2 and 32768^2).  The

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stddef.h>
 #include <stdint.h>
 
@@ -42,6 +44,22 @@ struct Geometry {
     int img_h() const { return img_height < 0 ? height : img_height; }
     int in_h() const { return in_rows < 0 ? height : in_rows; }
 };
+
+// cudaFuncSetAttribute is per device: `done` remembers, per call site, on
+// which devices (bit = ordinal) a kernel's dynamic shared-memory limit has
+// been raised, so contexts on several GPUs of one process all get it.
+template <typename F>
+inline cudaError_t ensure_smem(F* fn, size_t bytes, std::atomic<unsigned long long>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // Launch statistics (kernels issued) for instrumentation.
 struct LaunchCounter {
