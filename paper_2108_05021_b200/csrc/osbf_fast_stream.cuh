@@ -274,7 +274,10 @@ cudaError_t launch_stream(const PlaneView& in, const Geometry& g, double* out, s
     // split depends on the image height only, never on the batch size, so
     // results do not depend on how a batch is chunked.
     const int strips = (g.width + Ly::TWS - 1) / Ly::TWS;
-    const int band_rows = g.height < 512 ? g.height : 512;
+    // (r >= 10 runs two CTAs per SM, so whole 1024-row planes still leave
+    // a full last wave and save the second band's preamble)
+    const int band_rows = (R >= 10 && g.height <= 1024) ? g.height
+                                                        : (g.height < 512 ? g.height : 512);
     dim3 grid(strips, (g.height + band_rows - 1) / band_rows, g.batch);
     fast_stream_step<R, T, EXACT_DIV><<<grid, Ly::NTS, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                       band_of(g), band_rows);
