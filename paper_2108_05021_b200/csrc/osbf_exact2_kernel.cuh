@@ -69,11 +69,13 @@ constexpr int BR = 32;   // rows per block (radii <= 8; larger radii use 16, see
 constexpr int NT = 256;  // threads per strip CTA
 constexpr int NTK1 = 64; // threads per carry CTA (2 warps, 32 rows each)
 
-template <int R, int NUBV = 3>
+template <int R, int NUBV = 3, bool SP = false>
 struct XLay {
+    static constexpr int RAD = R;
     // rows per block: 16 above r=8 halves the U / row-sum / ring footprint
-    // (r=16: 149 KB -> 74 KB, one CTA per SM -> three)
-    static constexpr int BR = R > 8 ? 16 : ex2::BR;
+    // (r=16: 149 KB -> 74 KB, one CTA per SM -> three); the single-phase
+    // schedule (SP) always uses 16
+    static constexpr int BR = (SP || R > 8) ? 16 : ex2::BR;
     // staged U columns: [xs, xs + NU) with xs = floor((X0-R)/SW)*SW >= X0-R-SW+1,
     // covering up to X0 + TW + R - 1
     static constexpr int NU = TW + 2 * R + SW;
@@ -82,8 +84,10 @@ struct XLay {
     static constexpr int PUB = (NU % 4 == 2) ? NU : NU + 2;
     static constexpr int NCC = TW + 2 * R + 1;  // table columns cx in [X0-R, X0+TW+R]
     static constexpr int PR = NCC | 1;
-    // table rows kept: [y0-BR-R, y0+BR] (2BR+R+1 rows), as a power of two
-    static constexpr int NRING = (2 * BR + R + 2) <= 64 ? 64 : ((2 * BR + R + 2) <= 128 ? 128 : 256);
+    // table rows kept: [y0-BR-R, y0+BR] (2BR+R+1 rows; SP: one more block),
+    // as a power of two
+    static constexpr int SPAN = (SP ? 3 : 2) * BR + R + 2;
+    static constexpr int NRING = SPAN <= 64 ? 64 : (SPAN <= 128 ? 128 : 256);
     static constexpr int U_ELEMS = BR * PUB;
     // row segments of SW columns between stored carries (RR parallelism)
     static constexpr int NSEGR = (NU + SW - 1) / SW;
@@ -96,15 +100,17 @@ struct XLay {
     // staged-carry buffers: blocks k+1 .. k+NUB-1 can be in flight, i.e.
     // NUB-1 of them (2 for the stencil strips, which keeps r=8 at two CTAs
     // per SM)
-    static constexpr int NCS = NUB - 1;
-    static constexpr size_t SMEM = sizeof(double) * (NUB * static_cast<size_t>(U_ELEMS) + BR * PR +
-                                                     NRING * NCC + NCS * BR * NSEGR);
+    static constexpr int NCS = SP ? 3 : NUB - 1;
+    static constexpr int NRB = SP ? 2 : 1;  // row-sum buffers (SP: double-buffered)
+    static constexpr size_t SMEM = sizeof(double) * (NUB * static_cast<size_t>(U_ELEMS) +
+                                                     NRB * BR * PR + NRING * NCC +
+                                                     NCS * BR * NSEGR);
     // warps: column chains on [0, CCW), the early stencil rows on the rest;
     // row prefixes on [0, RRW), the late stencil rows on the rest
     static constexpr int CCW = (NCC + 31) / 32;
     static constexpr int RRW = (NSEGR * BR + 31) / 32;
     static_assert(CCW < NT / 32 && RRW < NT / 32, "no warps left for the stencil");
-    static_assert(2 * BR + R + 1 <= NRING, "table ring too small");
+    static_assert(SPAN <= NRING, "table ring too small");
 };
 
 }  // namespace ex2
@@ -199,13 +205,12 @@ __global__ void __launch_bounds__(WARPS * 32)
 
 // ---------------------------------------------------------------------------
 // K2: fused strip kernel (see the header comment).
-template <int R, typename T>
+template <typename L, typename T>
 __device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pitch,
                                             const double* __restrict__ carries, int nsc, int s0,
                                             long long gbase, int xs, int y0, int W, int H,
                                             double* __restrict__ U, double* __restrict__ cs,
                                             bool aligned16) {
-    using L = XLay<R>;
     constexpr int BR = L::BR;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if constexpr (sizeof(T) == 8) {
@@ -254,19 +259,19 @@ __device__ __forceinline__ void stage_block(const T* __restrict__ src, size_t pi
     cp_commit();
 }
 
-template <int R>
+template <typename L>
 __device__ __forceinline__ int ring_row(int cy) {
-    return cy & (XLay<R>::NRING - 1);
+    return cy & (L::NRING - 1);
 }
 
 // Stencil of rows [yb, yb + nrows) for output column x (lane-owned).  SAFE:
 // every table value of the strip so far passed table_value_safe.
-template <int R, bool SAFE>
+template <typename L, bool SAFE>
 __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
                                              const double* __restrict__ U, int xs, int X0, int yb,
                                              int r_lo, int r_hi, int w_first, int n_w, int W,
                                              int H, double* __restrict__ outp, size_t opitch) {
-    using L = XLay<R>;
+    constexpr int R = L::RAD;
     const int lx = threadIdx.x & 31, grp = (threadIdx.x >> 5) - w_first;
     const int x = X0 + lx;
     if (x >= W || grp < 0 || grp >= n_w) return;
@@ -283,10 +288,10 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
         double best = 0.0, best_abs = __longlong_as_double(0x7ff0000000000000LL);
         if (col_int && y >= R && y + R < H) {
             // 4x4 corner grid: rows {y-R, y, y+1, y+R+1}, cols {x-R, x, x+1, x+R+1}
-            const double* rp[4] = {Cr + ring_row<R>(y - R) * L::NCC + lx,
-                                   Cr + ring_row<R>(y) * L::NCC + lx,
-                                   Cr + ring_row<R>(y + 1) * L::NCC + lx,
-                                   Cr + ring_row<R>(y + R + 1) * L::NCC + lx};
+            const double* rp[4] = {Cr + ring_row<L>(y - R) * L::NCC + lx,
+                                   Cr + ring_row<L>(y) * L::NCC + lx,
+                                   Cr + ring_row<L>(y + 1) * L::NCC + lx,
+                                   Cr + ring_row<L>(y + R + 1) * L::NCC + lx};
             constexpr int co[4] = {0, R, R + 1, 2 * R + 1};
             double g[4][4];
 #pragma unroll
@@ -348,8 +353,8 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
                 const Win w = window(i, R);
                 const int x0 = max(x + w.u0, 0), x1 = min(x + w.u1, W - 1);
                 const int y0 = max(y + w.v0, 0), y1 = min(y + w.v1, H - 1);
-                const double* ra = Cr + ring_row<R>(y0) * L::NCC;
-                const double* rb = Cr + ring_row<R>(y1 + 1) * L::NCC;
+                const double* ra = Cr + ring_row<L>(y0) * L::NCC;
+                const double* rb = Cr + ring_row<L>(y1 + 1) * L::NCC;
                 const double A = rb[x1 + 1 - cbase], Bv = rb[x0 - cbase];
                 const double Cv = ra[x1 + 1 - cbase], D = ra[x0 - cbase];
                 const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(NT, 2)
     auto cs_of = [&](int k) { return cs + (k % L::NCS) * BR * L::NSEGR; };
     auto stage = [&](int k) {  // block k, or an empty group past the end
         if (k < nblocks)
-            stage_block<R, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + k * BR, W, H,
+            stage_block<L, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + k * BR, W, H,
                               U_of(k), cs_of(k), aligned16);
         else
             cp_commit();
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(NT, 2)
         if (y_walk0 > 0 && cx >= 0 && cx <= W)
             creg = ccar[(static_cast<size_t>(b) * nbands + band) * (W + 1) + cx];
         unsafe = !table_value_safe(creg);
-        Cr[ring_row<R>(y_walk0) * L::NCC + tid] = creg;  // table row y_walk0 (zero border at 0)
+        Cr[ring_row<L>(y_walk0) * L::NCC + tid] = creg;  // table row y_walk0 (zero border at 0)
     }
     stage(0);
     cp_wait<0>();
@@ -471,10 +476,10 @@ __global__ void __launch_bounds__(NT, 2)
         const int lo = max(r_from, y_out_lo - yb), hi = min(min(r_to, H - yb), y_out_hi - yb);
         if (lo >= hi) return;
         if (safe)
-            stencil_rows<R, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+            stencil_rows<L, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
                                   opitch);
         else
-            stencil_rows<R, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+            stencil_rows<L, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
                                    opitch);
     };
     for (int k = 0; k < nblocks; ++k) {
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(NT, 2)
                     for (int rr = 0; rr < nrows; ++rr) {
                         creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);  // above[x+1] + row
                         unsafe_here |= !table_value_safe(creg);
-                        Cr[ring_row<R>(y0 + rr + 1) * L::NCC + tid] = creg;
+                        Cr[ring_row<L>(y0 + rr + 1) * L::NCC + tid] = creg;
                     }
                 }
             }
@@ -523,6 +528,159 @@ __global__ void __launch_bounds__(NT, 2)
     if (!CARRIES) stencil_part(nblocks - 1, 0, BR, 0, NT / 32, !unsafe);
 }
 
+// Single-phase schedule (radius <= kSpMaxRadius, 16-row blocks): iteration
+// k runs, side by side with ONE barrier,
+//   column chains of block k          (CC warps; row sums of block k)
+//   row prefixes of block k+1         (RR warps; into the other row-sum buffer)
+//   stencil of block k-2, all rows    (every table row it needs was written
+//                                      by block k-1's chains; CC / RR warps
+//                                      join it once their chains are done)
+// Same adds, same table values, same stencil as exact_strip: bit-identical.
+// Used for 9 <= r <= 12, where it measured 5-11% faster than exact_strip
+// (5.25/5.65/5.53/5.50 -> 4.98/5.04/5.02/5.01 ms on C4); at r <= 8 it ties
+// or loses (the two-phase kernel's 32-row blocks amortise better), and
+// above 12 its table ring no longer fits two CTAs per SM.
+constexpr int kSpMinRadius = 9, kSpMaxRadius = 12;
+
+template <int R, typename T>
+__global__ void __launch_bounds__(NT, 2)
+    exact_strip_sp(const T* __restrict__ in, size_t pitch, size_t plane,
+                   const double* __restrict__ carries, int nsc, double* __restrict__ out,
+                   size_t opitch, size_t oplane, int W, int H, int band_h,
+                   const double* __restrict__ ccar) {
+    using L = XLay<R, 5, true>;
+    constexpr int BR = L::BR;
+    constexpr int CO = XLay<R, 6>::BR;  // the carries pass stores table rows band*band_h - CO
+    extern __shared__ double sm[];
+    double* Ubuf = sm;                              // NUB x [BR][PUB]
+    double* Rb0 = sm + L::NUB * L::U_ELEMS;          // 2 x [BR][PR] row sums
+    double* Cr = Rb0 + 2 * BR * L::PR;               // [NRING][NCC] table rows
+    double* cs = Cr + L::NRING * L::NCC;             // NCS x [NSEGR][BR] staged carries
+    const int b = blockIdx.y;
+    const int X0 = blockIdx.x * TW;
+    const int xs_raw = X0 - R;
+    const int xs = xs_raw <= 0 ? 0 : (xs_raw / SW) * SW;
+    const int s0 = xs / SW;
+    const T* src = in + static_cast<size_t>(b) * plane;
+    double* outp = out + static_cast<size_t>(b) * oplane;
+    const long long gbase = static_cast<long long>(b) * H;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int nbands = band_h > 0 ? (H + band_h - 1) / band_h : 1;
+    const int band = blockIdx.z;
+    int y_out_lo = 0, y_out_hi = H, y_walk0 = 0, y_walk_end = H;
+    if (band_h > 0) {
+        y_out_lo = band * band_h;
+        y_out_hi = min(H, y_out_lo + band_h);
+        y_walk0 = band == 0 ? 0 : y_out_lo - CO;
+        y_walk_end = min(H, y_out_hi + BR);
+    }
+    const int nblocks = (y_walk_end - y_walk0 + BR - 1) / BR;
+    const int xe = min(X0 + TW + R - 1, W - 1);
+    const bool aligned16 = sizeof(T) == 8 && (pitch % 2 == 0) &&
+                           (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    auto U_of = [&](int k) { return Ubuf + (k % L::NUB) * L::U_ELEMS; };
+    auto cs_of = [&](int k) { return cs + (k % L::NCS) * BR * L::NSEGR; };
+    auto Rb_of = [&](int k) { return Rb0 + (k & 1) * BR * L::PR; };
+    auto stage = [&](int k) {
+        if (k < nblocks)
+            stage_block<L, T>(src, pitch, carries, nsc, s0, gbase, xs, y_walk0 + k * BR, W, H,
+                              U_of(k), cs_of(k), aligned16);
+        else
+            cp_commit();
+    };
+    auto row_prefix = [&](int k, int t) {  // t: thread index within the RR warps
+        if (t >= BR * L::NSEGR) return;
+        const int rr = t % BR, seg = t / BR;
+        const double* u = U_of(k) + rr * L::PUB;
+        const double* c = cs_of(k);
+        double* rb = Rb_of(k) + rr * L::PR;
+        const int jbase = X0 - R - 1;
+        if (seg == 0) {
+            const int jfirst = xs - 1 - jbase;
+            for (int j = 0; j < jfirst && j < L::NCC; ++j) rb[j] = 0.0;
+            if (jfirst >= 0 && jfirst < L::NCC) rb[jfirst] = c[rr];
+        }
+        const int xa = xs + seg * SW;
+        double acc = c[seg * BR + rr];
+#pragma unroll
+        for (int i = 0; i < SW; ++i) {
+            const int x = xa + i;
+            if (x <= xe) {
+                acc = __dadd_rn(acc, u[seg * SW + i]);  // row += src[x]
+                const int j = x - jbase;
+                if (j >= 0 && j < L::NCC) rb[j] = acc;
+            }
+        }
+    };
+    auto stencil_part = [&](int j, int r_from, int r_to, int w_first, int n_w, bool safe) {
+        if (j < 0) return;
+        const int yb = y_walk0 + j * BR;
+        const int lo = max(r_from, y_out_lo - yb), hi = min(min(r_to, H - yb), y_out_hi - yb);
+        if (lo >= hi) return;
+        if (safe)
+            stencil_rows<L, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+                                  opitch);
+        else
+            stencil_rows<L, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
+                                   opitch);
+    };
+
+    double creg = 0.0;
+    bool unsafe = false;
+    if (tid < L::NCC) {
+        const int cx = X0 - R + tid;
+        if (y_walk0 > 0 && cx >= 0 && cx <= W)
+            creg = ccar[(static_cast<size_t>(b) * nbands + band) * (W + 1) + cx];
+        unsafe = !table_value_safe(creg);
+        Cr[ring_row<L>(y_walk0) * L::NCC + tid] = creg;
+    }
+    stage(0);
+    stage(1);
+    stage(2);
+    cp_wait<1>();  // blocks 0 and 1
+    __syncthreads();
+    row_prefix(0, tid);
+    unsafe = __syncthreads_or(unsafe);
+    // warps: [0, CCW) chains, [CCW, CCW+RRW) row prefixes, the rest stencil
+    // rows [0, SPLIT) of block k-2; chain warps then take rows [SPLIT, BR)
+    constexpr int CCW = L::CCW, RRW = L::RRW, NCH = CCW + RRW;
+    constexpr int NST = NT / 32 - NCH;
+    static_assert(NST >= 2, "no warps left for the stencil");
+    constexpr int SPLIT = 12;  // measured best of 4..16 at r = 2, 8, 9..12
+    for (int k = 0; k < nblocks; ++k) {
+        const int y0 = y_walk0 + k * BR;
+        const int nrows = min(BR, H - y0);
+        const bool safe = !unsafe;  // covers every chain up to block k-1
+        if (warp < CCW) {
+            bool unsafe_here = false;
+            if (tid < L::NCC) {
+                const int cx = X0 - R + tid;
+                const double* rb = Rb_of(k);
+                if (cx >= 0 && cx <= W) {
+                    for (int rr = 0; rr < nrows; ++rr) {
+                        creg = __dadd_rn(creg, rb[rr * L::PR + tid]);  // above[x+1] + row
+                        unsafe_here |= !table_value_safe(creg);
+                        Cr[ring_row<L>(y0 + rr + 1) * L::NCC + tid] = creg;
+                    }
+                }
+            }
+            unsafe |= unsafe_here;
+            stencil_part(k - 2, SPLIT, BR, 0, NCH, safe);
+        } else if (warp < NCH) {
+            if (k + 1 < nblocks) row_prefix(k + 1, tid - CCW * 32);
+            stencil_part(k - 2, SPLIT, BR, 0, NCH, safe);
+        } else {
+            stencil_part(k - 2, 0, SPLIT, NCH, NST, safe);
+        }
+        cp_wait<0>();  // block k+2 staged (for the row prefixes of the next iteration)
+        unsafe = __syncthreads_or(unsafe);
+        stage(k + 3);  // into block k-2's buffer, whose stencil just finished
+    }
+    // the last two blocks' stencils (their table rows are all written)
+    stencil_part(nblocks - 2, 0, BR, 0, NT / 32, !unsafe);
+    stencil_part(nblocks - 1, 0, BR, 0, NT / 32, !unsafe);
+}
+
 }  // namespace ex2
 
 // One radius (instantiated in osbf_exact2_rNN.cu).
@@ -547,6 +705,19 @@ cudaError_t exact2_launch_radius(const PlaneView& in, const Geometry& g, double*
                 band_h, ccar);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
+        }
+        if constexpr (R >= ex2::kSpMinRadius && R <= ex2::kSpMaxRadius) {
+            {
+                using LS = ex2::XLay<R, 5, true>;
+                static std::atomic<unsigned long long> done_sp{0};
+                if (cudaError_t e = ensure_smem(ex2::exact_strip_sp<R, T>, LS::SMEM, done_sp))
+                    return e;
+                ex2::exact_strip_sp<R, T>
+                    <<<dim3(strips, g.batch, nbands), ex2::NT, LS::SMEM, s>>>(
+                        base, in.pitch, in.plane, carries, nsc, out, opitch, oplane, g.width,
+                        g.height, nbands > 1 ? band_h : 0, ccar);
+                return cudaGetLastError();
+            }
         }
         ex2::exact_strip<R, T, false><<<dim3(strips, g.batch, nbands), ex2::NT, L::SMEM, s>>>(
             base, in.pitch, in.plane, carries, nsc, out, opitch, oplane, g.width, g.height,
