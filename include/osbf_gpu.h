@@ -136,6 +136,17 @@ osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
                               int batch, int radius, int iterations, void* stream);
 
 /*
+ * The classical box filter (filters2d.hpp:38-56), bit-identical: per
+ * iteration the whole-image SAT in the reference's order and the
+ * valid-count mean of the clipped (2r+1)^2 window.  Same conventions and
+ * error order as osbf_gpu_fast_osbf (radius checked first).
+ */
+osbf_status osbf_gpu_box_filter(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                               size_t in_pitch, size_t in_plane_stride, double* d_out,
+                               size_t out_pitch, size_t out_plane_stride, int width, int height,
+                               int batch, int radius, int iterations, void* stream);
+
+/*
  * Whole-image summed-area table, bit-identical to SummedAreaTable
  * (integral.hpp:16-30): d_cumsum is fp64 [batch][height+1][width+1].
  */
@@ -201,6 +212,16 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
 osbf_status osbf_gpu_fast_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
                                     double* h_out, int width, int height, int batch, int radius,
                                     int iterations);
+
+/* osbf::box_filter on host memory (batch planes back to back). */
+osbf_status osbf_gpu_box_filter_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                                     double* h_out, int width, int height, int batch, int radius,
+                                     int iterations);
+
+/* osbf::filter_multichannel with FilterVariant::Box (filters2d.hpp:379). */
+osbf_status osbf_gpu_filter_multichannel_box_host(osbf_ctx* ctx, const double* const* h_in,
+                                                  double* const* h_out, int channels, int width,
+                                                  int height, int radius, int iterations);
 
 /* osbf::filter_multichannel with FilterVariant::OsbfFast (filters2d.hpp:386):
  * fast_osbf on every channel (one batched launch per pass). */

@@ -66,6 +66,7 @@ class Oracle:
         lib.oracle_subwindow_means.argtypes = [_dp] + [ctypes.c_int] * 5 + [_dp]
         lib.oracle_sub_windows.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         lib.oracle_fast_osbf.argtypes = lib.oracle_osbf.argtypes
+        lib.oracle_box_filter.argtypes = lib.oracle_osbf.argtypes
         self.lib = lib
 
     def sub_windows(self, r: int):
@@ -82,6 +83,16 @@ class Oracle:
         st = self.lib.oracle_osbf_mt(_ptr(p), _ptr(out), w, h, r, iterations, threads)
         if st:
             raise CheckerError(st, "osbf")
+        return out
+
+    def box_filter(self, plane, r: int, iterations: int) -> np.ndarray:
+        """filters2d.hpp:38-56."""
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.oracle_box_filter(_ptr(p), _ptr(out), w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "box_filter")
         return out
 
     def fast_osbf(self, plane, r: int, iterations: int) -> np.ndarray:
@@ -139,6 +150,7 @@ class Reference:
         lib.ref_filter_multichannel_fast.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
         lib.ref_fast_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int]
+        lib.ref_box_filter.argtypes = lib.ref_fast_osbf.argtypes
         lib.ref_sat.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_subwindow_means.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _u8p]
         lib.ref_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
@@ -188,6 +200,15 @@ class Reference:
         st = fn(_ptr(p), _ptr(out), c, w, h, r, iterations)
         if st:
             raise CheckerError(st, "ref filter_multichannel")
+        return out
+
+    def box_filter(self, plane, r: int, iterations: int) -> np.ndarray:
+        p = _as_f64(plane)
+        h, w = p.shape
+        out = np.empty_like(p)
+        st = self.lib.ref_box_filter(_ptr(p), _ptr(out), w, h, r, iterations)
+        if st:
+            raise CheckerError(st, "ref box_filter")
         return out
 
     def fast_osbf(self, plane, r: int, iterations: int) -> np.ndarray:

@@ -252,3 +252,32 @@ int oracle_fast_osbf(const double* in, double* out, int w, int h, int r, int ite
     free(cur); free(nxt); free(q); free(c);
     return ORACLE_OK;
 }
+
+/* filters2d.hpp:38-56 (box_filter): rect_mean (integral.hpp:64-69) of the
+ * clipped window [x-r, x+r] x [y-r, y+r], iterated. */
+int oracle_box_filter(const double* in, double* out, int w, int h, int r, int iterations) {
+    if (r < 1) return ORACLE_ERR_INVALID_ARGUMENT;          /* :39-40 */
+    if (iterations < 0) return ORACLE_ERR_INVALID_ARGUMENT; /* :41-42 */
+    if (w < 1 || h < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h;
+    double* cur = (double*)malloc(sizeof(double) * n);
+    double* nxt = (double*)malloc(sizeof(double) * n);
+    double* c = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1));
+    if (!cur || !nxt || !c) {
+        free(cur); free(nxt); free(c);
+        return ORACLE_ERR_INVALID_ARGUMENT;
+    }
+    memcpy(cur, in, sizeof(double) * n);
+    for (int it = 0; it < iterations; ++it) {
+        oracle_sat_build(cur, w, h, c);
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x)
+                oracle_rect_mean(c, w, h, x - r, y - r, x + r, y + r, &nxt[(size_t)y * w + x]);
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    memcpy(out, cur, sizeof(double) * n);
+    free(cur); free(nxt); free(c);
+    return ORACLE_OK;
+}

@@ -65,6 +65,11 @@ int oracle_osbf_mt(const double* in, double* out, int w, int h, int r, int itera
  * |c - u|, output the candidate.  r < 1 is rejected even for 0 iterations. */
 int oracle_fast_osbf(const double* in, double* out, int w, int h, int r, int iterations);
 
+/* filters2d.hpp:38-56: per iteration the valid-count mean of the clipped
+ * (2r+1)^2 window on the whole-image SAT.  r < 1 is rejected even for 0
+ * iterations. */
+int oracle_box_filter(const double* in, double* out, int w, int h, int r, int iterations);
+
 #ifdef __cplusplus
 }
 #endif

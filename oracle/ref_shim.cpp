@@ -54,6 +54,17 @@ int ref_osbf(const double* in, double* out, int w, int h, int r, int iterations)
     }
 }
 
+// osbf::box_filter (filters2d.hpp:38-56)
+int ref_box_filter(const double* in, double* out, int w, int h, int r, int iterations) {
+    try {
+        const auto res = osbf::box_filter(to_plane(in, w, h), r, iterations);
+        std::memcpy(out, res.samples().data(), sizeof(double) * res.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // osbf::fast_osbf (filters2d.hpp:105-154, paper Algorithm 3)
 int ref_fast_osbf(const double* in, double* out, int w, int h, int r, int iterations) {
     try {

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     OsbfError,
     OutOfRange,
     SubWindowId,
+    box_filter,
     build_sat,
     default_context,
     fast_osbf,
@@ -30,7 +31,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "build", "lib", "Context", "default_context", "osbf", "osbf_step", "fast_osbf",
+    "build", "lib", "Context", "default_context", "osbf", "osbf_step", "fast_osbf", "box_filter",
     "filter_multichannel",
     "build_sat", "subwindow_means", "sub_windows", "SubWindowId", "FilterConfig", "FilterVariant",
     "set_max_threads", "max_threads", "OsbfError", "InvalidArgument", "DomainError", "OutOfRange",

@@ -44,6 +44,9 @@ SIGNATURES = [
     ("osbf_gpu_fast_osbf", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_void_p, _c_size, _c_size,
       _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),
+    ("osbf_gpu_box_filter", _c_int,
+     [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_void_p, _c_size, _c_size,
+      _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),
     ("osbf_gpu_subwindow_means", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_int, _c_int, _c_int, _c_int,
       _c_void_p, _c_void_p, _c_int, _c_void_p]),
@@ -65,6 +68,11 @@ SIGNATURES = [
       _c_int, _c_int, _c_int]),
     ("osbf_gpu_fast_osbf_host", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
+    ("osbf_gpu_box_filter_host", _c_int,
+     [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
+    ("osbf_gpu_filter_multichannel_box_host", _c_int,
+     [_c_void_p, ctypes.POINTER(_c_void_p), ctypes.POINTER(_c_void_p), _c_int, _c_int, _c_int,
+      _c_int, _c_int]),
     ("osbf_gpu_filter_multichannel_fast_host", _c_int,
      [_c_void_p, ctypes.POINTER(_c_void_p), ctypes.POINTER(_c_void_p), _c_int, _c_int, _c_int,
       _c_int, _c_int]),

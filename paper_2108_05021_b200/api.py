@@ -16,7 +16,8 @@ reference                              here
 ``osbf_step`` filters2d.hpp:61         :func:`osbf_step`
 ``osbf`` filters2d.hpp:91              :func:`osbf`
 ``fast_osbf`` filters2d.hpp:105        :func:`fast_osbf` (paper Algorithm 3, bit-identical)
-``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact, OsbfFast)
+``box_filter`` filters2d.hpp:38        :func:`box_filter` (bit-identical)
+``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact, OsbfFast, Box)
 ``set_max_threads`` parallel.hpp:20    :func:`set_max_threads` (no-op: the GPU
                                         result does not depend on any launch knob)
 =====================================  =============================================
@@ -206,6 +207,14 @@ class Context:
     def fast_osbf(self, src, radius: int, iterations: int, out=None, stream=None):
         """Paper Algorithm 3 (filters2d.hpp:105-154) over a CUDA tensor of shape
         (H, W) or (B, H, W); bit-identical to the reference's fast_osbf."""
+        return self._sat_filter("osbf_gpu_fast_osbf", src, radius, iterations, out, stream)
+
+    def box_filter(self, src, radius: int, iterations: int, out=None, stream=None):
+        """The classical box filter (filters2d.hpp:38-56) over a CUDA tensor;
+        bit-identical to the reference's box_filter."""
+        return self._sat_filter("osbf_gpu_box_filter", src, radius, iterations, out, stream)
+
+    def _sat_filter(self, fn, src, radius, iterations, out, stream):
         import torch
 
         x, batch, h, w = _as_batch(src)
@@ -217,7 +226,7 @@ class Context:
             out = out.view(batch, h, w)
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
-        _check(self._lib.osbf_gpu_fast_osbf(
+        _check(getattr(self._lib, fn)(
             self.handle, _dtype_code(x), ctypes.c_void_p(x.data_ptr()), x.stride(1), x.stride(0),
             ctypes.c_void_p(out.data_ptr()), out.stride(1), out.stride(0), w, h, batch, radius,
             iterations, ctypes.c_void_p(stream)))
@@ -309,8 +318,15 @@ class Context:
             w, h, batch, radius, iterations, _mode_code(mode)))
         return out
 
+    def box_filter_host(self, planes: np.ndarray, radius: int, iterations: int) -> np.ndarray:
+        """box_filter on host arrays (H, W) or (B, H, W)."""
+        return self._sat_filter_host("osbf_gpu_box_filter_host", planes, radius, iterations)
+
     def fast_osbf_host(self, planes: np.ndarray, radius: int, iterations: int) -> np.ndarray:
         """fast_osbf on host arrays (H, W) or (B, H, W): copy in, filter, copy out."""
+        return self._sat_filter_host("osbf_gpu_fast_osbf_host", planes, radius, iterations)
+
+    def _sat_filter_host(self, fn, planes, radius, iterations):
         p = np.ascontiguousarray(planes)
         code = {np.dtype(np.uint8): 0, np.dtype(np.float32): 1, np.dtype(np.float64): 2}.get(p.dtype)
         if code is None:
@@ -321,7 +337,7 @@ class Context:
         batch = 1 if p.ndim == 2 else p.shape[0]
         h, w = p.shape[-2:]
         out = np.empty(p.shape, dtype=np.float64)
-        _check(self._lib.osbf_gpu_fast_osbf_host(
+        _check(getattr(self._lib, fn)(
             self.handle, code, ctypes.c_void_p(p.ctypes.data), ctypes.c_void_p(out.ctypes.data),
             w, h, batch, radius, iterations))
         return out
@@ -352,6 +368,9 @@ class Context:
         ous = (ctypes.c_void_p * len(chans))(*[o.ctypes.data for o in outs])
         if variant is FilterVariant.OsbfFast:
             _check(self._lib.osbf_gpu_filter_multichannel_fast_host(
+                self.handle, ins, ous, len(chans), w, h, radius, iterations))
+        elif variant is FilterVariant.Box:
+            _check(self._lib.osbf_gpu_filter_multichannel_box_host(
                 self.handle, ins, ous, len(chans), w, h, radius, iterations))
         else:
             _check(self._lib.osbf_gpu_filter_multichannel_host(
@@ -438,11 +457,21 @@ def fast_osbf(plane, r: int, iterations: int):
     return default_context().fast_osbf_host(np.asarray(plane), r, iterations)
 
 
+def box_filter(plane, r: int, iterations: int):
+    """filters2d.hpp:38-56 — the classical box filter, bit-identical.  ``r < 1``
+    or ``iterations < 0`` raise InvalidArgument (the radius even for 0
+    iterations)."""
+    if _is_tensor(plane):
+        return default_context(plane.device.index or 0).box_filter(plane, r, iterations)
+    return default_context().box_filter_host(np.asarray(plane), r, iterations)
+
+
 def filter_multichannel(channels, config: FilterConfig, mode="exact"):
-    """filters2d.hpp:371-400, OsbfExact and OsbfFast branches: channels
+    """filters2d.hpp:371-400, OsbfExact / OsbfFast / Box branches: channels
     filtered independently (one batched launch per pass)."""
     config.validate()
-    if config.variant not in (FilterVariant.OsbfExact, FilterVariant.OsbfFast):
+    if config.variant not in (FilterVariant.OsbfExact, FilterVariant.OsbfFast,
+                              FilterVariant.Box):
         raise InvalidArgument(
             f"filter_multichannel: variant {config.variant.name} is not on the GPU OSBF path")
     chans = list(channels) if not (hasattr(channels, "ndim") and channels.ndim == 3) else channels
@@ -455,6 +484,8 @@ def filter_multichannel(channels, config: FilterConfig, mode="exact"):
         ctx = default_context(stack.device.index or 0)
         if config.variant is FilterVariant.OsbfFast:
             return ctx.fast_osbf(stack, config.radius, config.iterations)
+        if config.variant is FilterVariant.Box:
+            return ctx.box_filter(stack, config.radius, config.iterations)
         return ctx.iterate(stack, config.radius, config.iterations, mode)
     return default_context().filter_multichannel_host(chans, config.radius, config.iterations,
                                                       mode, variant=config.variant)

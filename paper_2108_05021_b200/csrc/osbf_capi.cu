@@ -477,14 +477,24 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
     return run_graphed(ctx, key, s, body);
 }
 
-osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
-                              size_t in_pitch, size_t in_plane_stride, double* d_out,
-                              size_t out_pitch, size_t out_plane_stride, int width, int height,
-                              int batch, int radius, int iterations, void* stream) {
+}  // extern "C"
+
+namespace {
+// The SAT-based companions of the OSBF path (fast_osbf, box_filter): the
+// reference checks the radius before the iteration count, even for 0
+// iterations (filters2d.hpp:39-42, :107-110), then iterates a pass that
+// rebuilds the whole-image table (bit-identical order) every iteration.
+enum class SatFilter { FastOsbf = 2, Box = 3 };
+
+osbf_status sat_filter(osbf_ctx* ctx, SatFilter which, osbf_dtype in_dtype, const void* d_in,
+                       size_t in_pitch, size_t in_plane_stride, double* d_out, size_t out_pitch,
+                       size_t out_plane_stride, int width, int height, int batch, int radius,
+                       int iterations, void* stream) {
+    const char* name = which == SatFilter::Box ? "box_filter" : "fast_osbf";
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
-    // filters2d.hpp:107-110: the radius is checked first, even for 0 iterations
-    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: radius must be >= 1");
-    if (iterations < 0) return fail(OSBF_ERR_INVALID_ARGUMENT, "fast_osbf: iterations must be >= 0");
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "%s: radius must be >= 1", name);
+    if (iterations < 0)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "%s: iterations must be >= 0", name);
     osbf_status st;
     if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
     if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
@@ -513,20 +523,43 @@ osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d
             [](int) { return 1; },
             [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int,
                 bool*) -> osbf_status {
-                OSBF_CUDA(osbf_gpu::fastosbf_pass(src, g, radius, ctx->rowpfx.as<double>(),
-                                                  ctx->sat.as<double>(), dst, dp, dpl, st_,
-                                                  ctx->lc),
-                          "fast_osbf pass");
+                auto pass = which == SatFilter::Box ? osbf_gpu::boxfilter_pass
+                                                    : osbf_gpu::fastosbf_pass;
+                OSBF_CUDA(pass(src, g, radius, ctx->rowpfx.as<double>(), ctx->sat.as<double>(),
+                               dst, dp, dpl, st_, ctx->lc),
+                          name);
                 return OSBF_OK;
             });
     };
     const std::vector<uintptr_t> key = {
-        2, static_cast<uintptr_t>(in_dtype), reinterpret_cast<uintptr_t>(d_in), in_pitch,
-        in_plane_stride, reinterpret_cast<uintptr_t>(d_out), out_pitch, out_plane_stride,
+        static_cast<uintptr_t>(which), static_cast<uintptr_t>(in_dtype),
+        reinterpret_cast<uintptr_t>(d_in), in_pitch, in_plane_stride,
+        reinterpret_cast<uintptr_t>(d_out), out_pitch, out_plane_stride,
         static_cast<uintptr_t>(width), static_cast<uintptr_t>(height),
         static_cast<uintptr_t>(batch), static_cast<uintptr_t>(radius),
         static_cast<uintptr_t>(iterations)};
     return run_graphed(ctx, key, s, body);
+}
+}  // namespace
+
+extern "C" {
+
+osbf_status osbf_gpu_fast_osbf(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                              size_t in_pitch, size_t in_plane_stride, double* d_out,
+                              size_t out_pitch, size_t out_plane_stride, int width, int height,
+                              int batch, int radius, int iterations, void* stream) {
+    return sat_filter(ctx, SatFilter::FastOsbf, in_dtype, d_in, in_pitch, in_plane_stride, d_out,
+                      out_pitch, out_plane_stride, width, height, batch, radius, iterations,
+                      stream);
+}
+
+osbf_status osbf_gpu_box_filter(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
+                               size_t in_pitch, size_t in_plane_stride, double* d_out,
+                               size_t out_pitch, size_t out_plane_stride, int width, int height,
+                               int batch, int radius, int iterations, void* stream) {
+    return sat_filter(ctx, SatFilter::Box, in_dtype, d_in, in_pitch, in_plane_stride, d_out,
+                      out_pitch, out_plane_stride, width, height, batch, radius, iterations,
+                      stream);
 }
 
 osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
@@ -738,6 +771,25 @@ osbf_status osbf_gpu_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h
                       });
 }
 
+osbf_status osbf_gpu_box_filter_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
+                                     double* h_out, int width, int height, int batch, int radius,
+                                     int iterations) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "box_filter: radius must be >= 1");
+    if (iterations < 0)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "box_filter: iterations must be >= 0");
+    osbf_status st;
+    if ((st = check_geometry(width, height, batch)) != OSBF_OK) return st;
+    if ((st = check_dtype(in_dtype)) != OSBF_OK) return st;
+    const size_t plane = static_cast<size_t>(width) * height;
+    return host_batch(ctx, in_dtype, h_in, h_out, width, height, batch,
+                      [&](const void* din, double* dout, int nb) {
+                          return osbf_gpu_box_filter(ctx, in_dtype, din, width, plane, dout, width,
+                                                     plane, width, height, nb, radius, iterations,
+                                                     ctx->stream);
+                      });
+}
+
 osbf_status osbf_gpu_fast_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
                                     double* h_out, int width, int height, int batch, int radius,
                                     int iterations) {
@@ -769,7 +821,7 @@ namespace {
 // are independent, so they run as one batched launch per pass.
 osbf_status multichannel_host(osbf_ctx* ctx, const double* const* h_in, double* const* h_out,
                               int channels, int width, int height, int radius, int iterations,
-                              bool fast_variant, osbf_mode mode) {
+                              int variant, osbf_mode mode) {  // 0 OsbfExact, 1 OsbfFast, 2 Box
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
     // FilterConfig::validate (core.hpp:244-253), then the channel checks of
     // MultiChannelImage (core.hpp:85-92).
@@ -795,10 +847,14 @@ osbf_status multichannel_host(osbf_ctx* ctx, const double* const* h_in, double* 
                   "H2D");
     }
     // Channels are independent (filters2d.hpp:376-384): one batched launch.
-    st = fast_variant ? osbf_gpu_fast_osbf(ctx, OSBF_F64, din, width, plane, dout, width, plane,
-                                           width, height, channels, radius, iterations, s)
-                      : osbf_gpu_iterate(ctx, OSBF_F64, din, width, plane, dout, width, plane,
-                                         width, height, channels, radius, iterations, mode, s);
+    st = variant == 1   ? osbf_gpu_fast_osbf(ctx, OSBF_F64, din, width, plane, dout, width,
+                                             plane, width, height, channels, radius,
+                                             iterations, s)
+         : variant == 2 ? osbf_gpu_box_filter(ctx, OSBF_F64, din, width, plane, dout, width,
+                                              plane, width, height, channels, radius,
+                                              iterations, s)
+                        : osbf_gpu_iterate(ctx, OSBF_F64, din, width, plane, dout, width, plane,
+                                           width, height, channels, radius, iterations, mode, s);
     if (st != OSBF_OK) return st;
     for (int c = 0; c < channels; ++c)
         OSBF_CUDA(cudaMemcpyAsync(h_out[c], dout + c * plane, plane * sizeof(double),
@@ -816,14 +872,21 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
                                               double* const* h_out, int channels, int width,
                                               int height, int radius, int iterations,
                                               osbf_mode mode) {
-    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, false,
+    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, 0,
                              mode);
 }
 
 osbf_status osbf_gpu_filter_multichannel_fast_host(osbf_ctx* ctx, const double* const* h_in,
                                                    double* const* h_out, int channels, int width,
                                                    int height, int radius, int iterations) {
-    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, true,
+    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, 1,
+                             OSBF_MODE_EXACT);
+}
+
+osbf_status osbf_gpu_filter_multichannel_box_host(osbf_ctx* ctx, const double* const* h_in,
+                                                  double* const* h_out, int channels, int width,
+                                                  int height, int radius, int iterations) {
+    return multichannel_host(ctx, h_in, h_out, channels, width, height, radius, iterations, 2,
                              OSBF_MODE_EXACT);
 }
 

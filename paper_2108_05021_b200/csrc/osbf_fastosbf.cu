@@ -1,8 +1,8 @@
-// Paper Algorithm 3, the reference's fast_osbf (filters2d.hpp:105-154),
-// bit-identical.  Per iteration:
+// Paper Algorithm 3, the reference's fast_osbf (filters2d.hpp:105-154), and
+// the classical box filter (filters2d.hpp:38-56), both bit-identical.  Per iteration:
 //   1. the whole-image summed-area table in the reference's serial order
 //      (exact_build_sat, the same kernels the exact OSBF diagnostics use);
-//   2. fosbf_quarter: Q(x,y) = rect_mean(x-r, y-r, x, y) (filters2d.hpp:116-
+//   2. rect_mean_field: Q(x,y) = rect_mean(x-r, y-r, x, y) (filters2d.hpp:116-
 //      119): clipped ((A-B)-C)+D, one IEEE division by the clipped count
 //      (integral.hpp:41-69), written over the row-prefix workspace (free once
 //      the table exists);
@@ -15,22 +15,29 @@
 namespace osbf_gpu {
 namespace {
 
+// out(x,y) = rect_mean(x+dx0, y+dy0, x+dx1, y+dy1) on the table (clipped
+// ((A-B)-C)+D, one IEEE division by the clipped count, integral.hpp:41-69);
+// dx0, dy0 <= 0 <= dx1, dy1, so the clipped rectangle is never empty.
+// fast_osbf's quarter field (-r, -r, 0, 0) and box_filter's window
+// (-r, -r, r, r, filters2d.hpp:38-56).
 __global__ void __launch_bounds__(256)
-    fosbf_quarter(const double* __restrict__ sat, double* __restrict__ q, int W, int H, int r) {
+    rect_mean_field(const double* __restrict__ sat, double* __restrict__ q, size_t q_pitch,
+                    size_t q_plane, int W, int H, int dx0, int dy0, int dx1, int dy1) {
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int b = blockIdx.z;
     if (x >= W || y >= H) return;
     const long long cols = static_cast<long long>(W) + 1;
     const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
-    const int x0 = max(x - r, 0), y0 = max(y - r, 0);  // x1 = x, y1 = y are in range
-    const long long n = static_cast<long long>(x - x0 + 1) * (y - y0 + 1);
-    const double A = C[(y + 1) * cols + (x + 1)];
-    const double Bv = C[(y + 1) * cols + x0];
-    const double Cv = C[y0 * cols + (x + 1)];
+    const int x0 = max(x + dx0, 0), y0 = max(y + dy0, 0);
+    const int x1 = min(x + dx1, W - 1), y1 = min(y + dy1, H - 1);
+    const long long n = static_cast<long long>(x1 - x0 + 1) * (y1 - y0 + 1);
+    const double A = C[(y1 + 1) * cols + (x1 + 1)];
+    const double Bv = C[(y1 + 1) * cols + x0];
+    const double Cv = C[y0 * cols + (x1 + 1)];
     const double D = C[y0 * cols + x0];
     const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
-    q[(static_cast<size_t>(b) * H + y) * W + x] = __ddiv_rn(s, static_cast<double>(n));
+    q[b * q_plane + static_cast<size_t>(y) * q_pitch + x] = __ddiv_rn(s, static_cast<double>(n));
 }
 
 template <typename T>
@@ -78,7 +85,9 @@ cudaError_t fastosbf_pass(const PlaneView& in, const Geometry& g, int radius, do
     cudaError_t e = exact_build_sat(in, g, rowpfx, sat, s, lc);
     if (e != cudaSuccess) return e;
     const dim3 grid((g.width + 31) / 32, (g.height + 7) / 8, g.batch);
-    fosbf_quarter<<<grid, 256, 0, s>>>(sat, rowpfx, g.width, g.height, radius);
+    rect_mean_field<<<grid, 256, 0, s>>>(sat, rowpfx, g.width,
+                                         static_cast<size_t>(g.width) * g.height, g.width,
+                                         g.height, -radius, -radius, 0, 0);
     ++lc.launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++lc.launches;
@@ -99,6 +108,18 @@ cudaError_t fastosbf_pass(const PlaneView& in, const Geometry& g, int radius, do
                                               g.width, g.height, radius);
             break;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t boxfilter_pass(const PlaneView& in, const Geometry& g, int radius, double* rowpfx,
+                           double* sat, double* out, size_t out_pitch, size_t out_plane,
+                           cudaStream_t s, LaunchCounter& lc) {
+    cudaError_t e = exact_build_sat(in, g, rowpfx, sat, s, lc);
+    if (e != cudaSuccess) return e;
+    const dim3 grid((g.width + 31) / 32, (g.height + 7) / 8, g.batch);
+    rect_mean_field<<<grid, 256, 0, s>>>(sat, out, out_pitch, out_plane, g.width, g.height,
+                                         -radius, -radius, radius, radius);
+    ++lc.launches;
     return cudaGetLastError();
 }
 

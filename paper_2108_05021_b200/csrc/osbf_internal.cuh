@@ -96,6 +96,12 @@ cudaError_t fastosbf_pass(const PlaneView& in, const Geometry& g, int radius, do
                           double* sat, double* out, size_t out_pitch, size_t out_plane,
                           cudaStream_t s, LaunchCounter& lc);
 
+// One box_filter iteration (filters2d.hpp:38-56), bit-identical: exact SAT,
+// then the valid-count mean of the clipped (2r+1)^2 window into out.
+cudaError_t boxfilter_pass(const PlaneView& in, const Geometry& g, int radius, double* rowpfx,
+                           double* sat, double* out, size_t out_pitch, size_t out_plane,
+                           cudaStream_t s, LaunchCounter& lc);
+
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
 // Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
 constexpr int kFastMaxRadius = 16;

@@ -50,6 +50,10 @@ def fastosbf_golden_cases():
     return sorted(glob.glob(os.path.join(GOLDEN_DIR, "fastosbf", "*.npz")))
 
 
+def boxfilter_golden_cases():
+    return sorted(glob.glob(os.path.join(GOLDEN_DIR, "boxfilter", "*.npz")))
+
+
 def load_golden(path):
     d = np.load(path)
     return {k: d[k] for k in d.files}

@@ -4,6 +4,7 @@
 // GPU through libosbf_gpu.so.  The CPU checker is the oracle restatement
 // (oracle/osbf_oracle.c; test infrastructure only).  Prints one PASS/FAIL
 // line per case; exit code = number of failures.
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -202,10 +203,16 @@ int main() {
                 if (!bit_equal(out.channel(c), osbf::osbf(rgb.channel(c), 2, 2))) return false;
             osbf::FilterConfig bad = cfg;
             bad.radius = 0;
+            osbf::FilterConfig generic = cfg;
+            generic.variant = osbf::FilterVariant::OneSidedGeneric;
             osbf::FilterConfig box = cfg;
             box.variant = osbf::FilterVariant::Box;
+            const auto boxed = osbf::filter_multichannel(rgb, box);
+            for (int c = 0; c < 3; ++c)
+                if (!bit_equal(boxed.channel(c), osbf::box_filter(rgb.channel(c), 2, 2)))
+                    return false;
             return throws<std::invalid_argument>([&] { osbf::filter_multichannel(rgb, bad); }) &&
-                   throws<std::invalid_argument>([&] { osbf::filter_multichannel(rgb, box); });
+                   throws<std::invalid_argument>([&] { osbf::filter_multichannel(rgb, generic); });
         });
         run(("outputs identical for any thread cap" + tag).c_str(), [] {
             const auto p = random_plane(33, 29, 123);
@@ -230,6 +237,42 @@ int main() {
             const auto p = random_plane(24, 24, 200 + r);
             if (max_abs_diff(osbf::osbf(p, r, 3), checker_osbf(p, r, 3)) > 1e-9) return false;
         }
+        return true;
+    });
+
+    // ---- box_filter: test_filters2d.cpp:44-69 (fixed points, oracle, errors)
+    run("box_filter bit-identical to the oracle; constant planes fixed; errors", [] {
+        const ImagePlane c(9, 7, 3.25);
+        for (int r : {1, 2, 5})
+            if (max_abs_diff(osbf::box_filter(c, r, 3), c) != 0.0) return false;
+        for (int r : {1, 2, 4, 9}) {
+            const auto p = random_plane(33, 21, 400 + r);
+            std::vector<double> want(p.size());
+            if (oracle_box_filter(p.samples().data(), want.data(), 33, 21, r, 3) != 0) return false;
+            const auto got = osbf::box_filter(p, r, 3);
+            if (std::memcmp(got.samples().data(), want.data(), sizeof(double) * want.size()) != 0)
+                return false;
+        }
+        const auto p = random_plane(8, 8, 2);
+        return bit_equal(osbf::box_filter(p, 2, 0), p) &&
+               throws<std::invalid_argument>([&] { osbf::box_filter(p, 0, 0); }) &&
+               throws<std::invalid_argument>([&] { osbf::box_filter(p, 2, -1); });
+    });
+
+    // ---- parallel.hpp: parallel_for_rows covers [0, count) in disjoint blocks
+    run("parallel_for_rows covers every row once for any thread cap", [] {
+        for (int cap : {0, 1, 3, 64}) {
+            osbf::set_max_threads(cap);
+            for (int count : {0, 1, 7, 100}) {
+                std::vector<std::atomic<int>> hits(static_cast<size_t>(count));
+                osbf::parallel_for_rows(count, [&](int b, int e) {
+                    for (int i = b; i < e; ++i) hits[static_cast<size_t>(i)]++;
+                });
+                for (auto& h : hits)
+                    if (h.load() != 1) return false;
+            }
+        }
+        osbf::set_max_threads(0);
         return true;
     });
 

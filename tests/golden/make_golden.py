@@ -100,6 +100,24 @@ def fast_osbf_cases():
     return out
 
 
+def box_filter_cases():
+    """(name, input, r, iterations) for box_filter (filters2d.hpp:38-56)."""
+    out = []
+    # test_filters2d.cpp:44-48 — constant planes are fixed points
+    for r in (1, 3):
+        out.append((f"constant_11x7_r{r}", np.full((7, 11), 42.0), r, 3))
+    # test_filters2d.cpp:50-69 — against the brute-force oracle, several radii
+    for r in (1, 2, 4, 9, 16):
+        out.append((f"random_45x31_r{r}", random_plane(31, 45, 500 + r), r, 3))
+    rng = np.random.default_rng(35)
+    out.append(("u8mosaic_r2", synth.u8_mosaic(96, 80, rng, block=(4, 40)), 2, 5))
+    out.append(("one_px", np.array([[7.5]]), 2, 3))
+    out.append(("row_1x17", random_plane(1, 17, 25), 3, 2))
+    out.append(("zero_iters", random_plane(10, 10, 23), 2, 0))
+    out.append(("c2_shrink12", synth.make_input("C2", shrink=12), 3, 2))
+    return out
+
+
 def main() -> None:
     ref = Reference()
     ref.set_max_threads(1)
@@ -122,6 +140,14 @@ def main() -> None:
         np.savez_compressed(os.path.join(HERE, "fastosbf", f"{name}.npz"), input=inp, output=out,
                             radius=r, iterations=iters)
         print(f"fastosbf/{name:20s} in {inp.shape} {inp.dtype} r={r} it={iters}")
+    os.makedirs(os.path.join(HERE, "boxfilter"), exist_ok=True)
+    for name, inp, r, iters in box_filter_cases():
+        x = inp.astype(np.float64)
+        out = (np.stack([ref.box_filter(c, r, iters) for c in x]) if x.ndim == 3
+               else ref.box_filter(x, r, iters))
+        np.savez_compressed(os.path.join(HERE, "boxfilter", f"{name}.npz"), input=inp,
+                            output=out, radius=r, iterations=iters)
+        print(f"boxfilter/{name:20s} in {inp.shape} {inp.dtype} r={r} it={iters}")
     # integral.hpp / test_integral.cpp:19-29 known SAT
     p = np.array([[1.0, 2.0], [3.0, 4.0]])
     np.savez_compressed(os.path.join(HERE, "sat_2x2.npz"), input=p, cumsum=ref.sat(p))

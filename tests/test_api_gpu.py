@@ -45,8 +45,12 @@ def test_multichannel_semantics():
         ob.filter_multichannel(rgb, ob.FilterConfig(radius=0))
     with pytest.raises(ob.InvalidArgument):
         ob.filter_multichannel(rgb * 2, cfg)  # 6 channels
-    with pytest.raises(ob.InvalidArgument):
-        ob.filter_multichannel(rgb, ob.FilterConfig(variant=ob.FilterVariant.Box))
+    with pytest.raises(ob.InvalidArgument):  # not on the GPU path
+        ob.filter_multichannel(rgb, ob.FilterConfig(variant=ob.FilterVariant.Gaussian))
+    boxed = ob.filter_multichannel(rgb, ob.FilterConfig(radius=2, iterations=2,
+                                                        variant=ob.FilterVariant.Box))
+    for f, c in zip(boxed, rgb):
+        assert np.array_equal(bits(f), bits(ob.box_filter(c, 2, 2)))
 
 
 def test_launch_counter_counts_kernels(ctx):
