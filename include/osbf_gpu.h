@@ -147,6 +147,19 @@ osbf_status osbf_gpu_box_filter(osbf_ctx* ctx, osbf_dtype in_dtype, const void* 
                                int batch, int radius, int iterations, void* stream);
 
 /*
+ * 3-D extension (filters3d.hpp:55-114): osbf_3d (14 one-sided regions) and
+ * box_filter_3d on one fp64 volume, samples x-fastest then y then z (the
+ * reference's Volume layout, core.hpp:148-150), bit-identical (the
+ * summed-volume table of integral.hpp:98-113 in the reference's order).
+ * radius < 1 is INVALID_ARGUMENT even for 0 iterations.
+ */
+osbf_status osbf_gpu_osbf_3d(osbf_ctx* ctx, const double* d_in, double* d_out, int width,
+                            int height, int depth, int radius, int iterations, void* stream);
+osbf_status osbf_gpu_box_filter_3d(osbf_ctx* ctx, const double* d_in, double* d_out, int width,
+                                  int height, int depth, int radius, int iterations,
+                                  void* stream);
+
+/*
  * Whole-image summed-area table, bit-identical to SummedAreaTable
  * (integral.hpp:16-30): d_cumsum is fp64 [batch][height+1][width+1].
  */
@@ -212,6 +225,13 @@ osbf_status osbf_gpu_filter_multichannel_host(osbf_ctx* ctx, const double* const
 osbf_status osbf_gpu_fast_osbf_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
                                     double* h_out, int width, int height, int batch, int radius,
                                     int iterations);
+
+/* osbf::osbf_3d / box_filter_3d on host memory (one volume). */
+osbf_status osbf_gpu_osbf_3d_host(osbf_ctx* ctx, const double* h_in, double* h_out, int width,
+                                 int height, int depth, int radius, int iterations);
+osbf_status osbf_gpu_box_filter_3d_host(osbf_ctx* ctx, const double* h_in, double* h_out,
+                                       int width, int height, int depth, int radius,
+                                       int iterations);
 
 /* osbf::box_filter on host memory (batch planes back to back). */
 osbf_status osbf_gpu_box_filter_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,

@@ -67,6 +67,10 @@ class Oracle:
         lib.oracle_sub_windows.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         lib.oracle_fast_osbf.argtypes = lib.oracle_osbf.argtypes
         lib.oracle_box_filter.argtypes = lib.oracle_osbf.argtypes
+        lib.oracle_svt_build.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
+        lib.oracle_svt_build.restype = None
+        lib.oracle_osbf_3d.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
+        lib.oracle_box_filter_3d.argtypes = lib.oracle_osbf_3d.argtypes
         self.lib = lib
 
     def sub_windows(self, r: int):
@@ -83,6 +87,29 @@ class Oracle:
         st = self.lib.oracle_osbf_mt(_ptr(p), _ptr(out), w, h, r, iterations, threads)
         if st:
             raise CheckerError(st, "osbf")
+        return out
+
+    # 3-D: volumes as numpy (D, H, W) arrays (x fastest)
+    def svt(self, vol) -> np.ndarray:
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        d, h, w = v.shape
+        c = np.empty((d + 1, h + 1, w + 1), dtype=np.float64)
+        self.lib.oracle_svt_build(_ptr(v), w, h, d, _ptr(c))
+        return c
+
+    def osbf_3d(self, vol, r: int, iterations: int) -> np.ndarray:
+        return self._f3(self.lib.oracle_osbf_3d, vol, r, iterations, "osbf_3d")
+
+    def box_filter_3d(self, vol, r: int, iterations: int) -> np.ndarray:
+        return self._f3(self.lib.oracle_box_filter_3d, vol, r, iterations, "box_filter_3d")
+
+    def _f3(self, fn, vol, r, iterations, name):
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        d, h, w = v.shape
+        out = np.empty_like(v)
+        st = fn(_ptr(v), _ptr(out), w, h, d, r, iterations)
+        if st:
+            raise CheckerError(st, name)
         return out
 
     def box_filter(self, plane, r: int, iterations: int) -> np.ndarray:
@@ -151,6 +178,8 @@ class Reference:
         lib.ref_fast_osbf.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int]
         lib.ref_box_filter.argtypes = lib.ref_fast_osbf.argtypes
+        lib.ref_filter_3d.argtypes = [_dp, _dp] + [ctypes.c_int] * 6
+        lib.ref_svt.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_sat.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_subwindow_means.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _u8p]
         lib.ref_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
@@ -200,6 +229,30 @@ class Reference:
         st = fn(_ptr(p), _ptr(out), c, w, h, r, iterations)
         if st:
             raise CheckerError(st, "ref filter_multichannel")
+        return out
+
+    def svt(self, vol) -> np.ndarray:
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        d, h, w = v.shape
+        c = np.empty((d + 1, h + 1, w + 1), dtype=np.float64)
+        st = self.lib.ref_svt(_ptr(v), w, h, d, _ptr(c))
+        if st:
+            raise CheckerError(st, "ref svt")
+        return c
+
+    def osbf_3d(self, vol, r: int, iterations: int) -> np.ndarray:
+        return self._f3(vol, r, iterations, 1)
+
+    def box_filter_3d(self, vol, r: int, iterations: int) -> np.ndarray:
+        return self._f3(vol, r, iterations, 0)
+
+    def _f3(self, vol, r, iterations, osbf3):
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        d, h, w = v.shape
+        out = np.empty_like(v)
+        st = self.lib.ref_filter_3d(_ptr(v), _ptr(out), w, h, d, r, iterations, osbf3)
+        if st:
+            raise CheckerError(st, "ref filter_3d")
         return out
 
     def box_filter(self, plane, r: int, iterations: int) -> np.ndarray:

@@ -281,3 +281,113 @@ int oracle_box_filter(const double* in, double* out, int w, int h, int r, int it
     free(cur); free(nxt); free(c);
     return ORACLE_OK;
 }
+
+/* ---- 3-D extension -------------------------------------------------------- */
+
+void oracle_svt_build(const double* vol, int w, int h, int d, double* c) {
+    const size_t W1 = (size_t)w + 1, H1 = (size_t)h + 1;
+    memset(c, 0, sizeof(double) * W1 * H1 * ((size_t)d + 1));
+#define T3(x, y, z) c[((size_t)(z) * H1 + (size_t)(y)) * W1 + (size_t)(x)]
+    for (int z = 0; z < d; ++z)
+        for (int y = 0; y < h; ++y) {
+            double row = 0.0;
+            for (int x = 0; x < w; ++x) {
+                row += vol[((size_t)z * h + y) * w + x];
+                /* integral.hpp:107-108, evaluated left to right */
+                T3(x + 1, y + 1, z + 1) =
+                    row + T3(x + 1, y, z + 1) + T3(x + 1, y + 1, z) - T3(x + 1, y, z);
+            }
+        }
+}
+
+/* integral.hpp:121-160 (box_sum / box_count / box_mean); 0 count -> 0.0 */
+static double box_mean3(const double* c, int w, int h, int d, int x0, int y0, int z0, int x1,
+                        int y1, int z1, int* empty) {
+    const size_t W1 = (size_t)w + 1, H1 = (size_t)h + 1;
+    x0 = imax(x0, 0); y0 = imax(y0, 0); z0 = imax(z0, 0);
+    x1 = imin(x1, w - 1); y1 = imin(y1, h - 1); z1 = imin(z1, d - 1);
+    if (x0 > x1 || y0 > y1 || z0 > z1) {
+        *empty = 1;
+        return 0.0;
+    }
+    const int ax = x0, bx = x1 + 1, ay = y0, by = y1 + 1, az = z0, bz = z1 + 1;
+    const double s = T3(bx, by, bz) - T3(ax, by, bz) - T3(bx, ay, bz) - T3(bx, by, az) +
+                     T3(ax, ay, bz) + T3(ax, by, az) + T3(bx, ay, az) - T3(ax, ay, az);
+    const long long n = (long long)(x1 - x0 + 1) * (y1 - y0 + 1) * (z1 - z0 + 1);
+    return s / (double)n;
+}
+#undef T3
+
+static void regions3(int r, int reg[14][6]) {
+    /* filters3d.hpp:29-51: octants by sign pattern, then -x,+x,-y,+y,-z,+z */
+    int id = 0;
+    for (int sz = 0; sz < 2; ++sz)
+        for (int sy = 0; sy < 2; ++sy)
+            for (int sx = 0; sx < 2; ++sx) {
+                int* g = reg[id++];
+                g[0] = sx ? 0 : -r; g[1] = sx ? r : 0;
+                g[2] = sy ? 0 : -r; g[3] = sy ? r : 0;
+                g[4] = sz ? 0 : -r; g[5] = sz ? r : 0;
+            }
+    const int half[6][6] = {{-r, 0, -r, r, -r, r}, {0, r, -r, r, -r, r}, {-r, r, -r, 0, -r, r},
+                            {-r, r, 0, r, -r, r},  {-r, r, -r, r, -r, 0}, {-r, r, -r, r, 0, r}};
+    for (int i = 0; i < 6; ++i)
+        for (int k = 0; k < 6; ++k) reg[8 + i][k] = half[i][k];
+}
+
+static int filter3(const double* in, double* out, int w, int h, int d, int r, int iters,
+                   int osbf) {
+    if (r < 1 || iters < 0 || w < 1 || h < 1 || d < 1) return ORACLE_ERR_INVALID_ARGUMENT;
+    const size_t n = (size_t)w * h * d;
+    double* cur = (double*)malloc(sizeof(double) * n);
+    double* nxt = (double*)malloc(sizeof(double) * n);
+    double* c = (double*)malloc(sizeof(double) * ((size_t)w + 1) * ((size_t)h + 1) * ((size_t)d + 1));
+    if (!cur || !nxt || !c) {
+        free(cur); free(nxt); free(c);
+        return ORACLE_ERR_INVALID_ARGUMENT;
+    }
+    int reg[14][6];
+    regions3(r, reg);
+    memcpy(cur, in, sizeof(double) * n);
+    for (int it = 0; it < iters; ++it) {
+        oracle_svt_build(cur, w, h, d, c);
+        for (int z = 0; z < d; ++z)
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x) {
+                    const size_t i = ((size_t)z * h + y) * w + x;
+                    int empty = 0;
+                    if (!osbf) {
+                        nxt[i] = box_mean3(c, w, h, d, x - r, y - r, z - r, x + r, y + r, z + r,
+                                           &empty);
+                        continue;
+                    }
+                    const double u = cur[i];
+                    double best = 0.0, best_abs = INFINITY;
+                    for (int k = 0; k < 14; ++k) {
+                        const double a = box_mean3(c, w, h, d, x + reg[k][0], y + reg[k][2],
+                                                   z + reg[k][4], x + reg[k][1], y + reg[k][3],
+                                                   z + reg[k][5], &empty);
+                        const double dist = fabs(a - u);
+                        if (dist < best_abs) {
+                            best_abs = dist;
+                            best = a;
+                        }
+                    }
+                    nxt[i] = best;
+                }
+        double* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    memcpy(out, cur, sizeof(double) * n);
+    free(cur); free(nxt); free(c);
+    return ORACLE_OK;
+}
+
+int oracle_box_filter_3d(const double* in, double* out, int w, int h, int d, int r, int iters) {
+    return filter3(in, out, w, h, d, r, iters, 0);
+}
+
+int oracle_osbf_3d(const double* in, double* out, int w, int h, int d, int r, int iters) {
+    return filter3(in, out, w, h, d, r, iters, 1);
+}

@@ -70,6 +70,16 @@ int oracle_fast_osbf(const double* in, double* out, int w, int h, int r, int ite
  * iterations. */
 int oracle_box_filter(const double* in, double* out, int w, int h, int r, int iterations);
 
+/* 3-D extension. Volumes are x-fastest, then y, then z.
+ * integral.hpp:98-113: summed-volume table with zero border slabs,
+ * cumsum[(z*(h+1)+y)*(w+1)+x], built with a running row sum per (y,z) row:
+ *   T(x+1,y+1,z+1) = ((row + T(x+1,y,z+1)) + T(x+1,y+1,z)) - T(x+1,y,z). */
+void oracle_svt_build(const double* vol, int w, int h, int d, double* cumsum);
+/* filters3d.hpp:55-76 (box_filter_3d) and :78-114 (osbf_3d, 14 regions,
+ * strict-< first minimum).  r < 1 / iterations < 0 are rejected. */
+int oracle_box_filter_3d(const double* in, double* out, int w, int h, int d, int r, int iters);
+int oracle_osbf_3d(const double* in, double* out, int w, int h, int d, int r, int iters);
+
 #ifdef __cplusplus
 }
 #endif

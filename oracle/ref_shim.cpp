@@ -13,6 +13,7 @@
 
 #include "osbf/bench.hpp"
 #include "osbf/filters2d.hpp"
+#include "osbf/filters3d.hpp"
 #include "osbf/parallel.hpp"
 
 namespace {
@@ -35,6 +36,10 @@ osbf::ImagePlane to_plane(const double* p, int w, int h) {
     return osbf::ImagePlane(w, h, std::vector<double>(p, p + static_cast<size_t>(w) * h));
 }
 
+osbf::Volume to_volume(const double* p, int w, int h, int d) {
+    return osbf::Volume(w, h, d, std::vector<double>(p, p + static_cast<size_t>(w) * h * d));
+}
+
 }  // namespace
 
 extern "C" {
@@ -48,6 +53,36 @@ int ref_osbf(const double* in, double* out, int w, int h, int r, int iterations)
     try {
         const auto res = osbf::osbf(to_plane(in, w, h), r, iterations);
         std::memcpy(out, res.samples().data(), sizeof(double) * res.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// osbf::osbf_3d / box_filter_3d (filters3d.hpp:55-114)
+int ref_filter_3d(const double* in, double* out, int w, int h, int d, int r, int iterations,
+                  int osbf3) {
+    try {
+        const auto v = to_volume(in, w, h, d);
+        const auto res = osbf3 ? osbf::osbf_3d(v, r, iterations) : osbf::box_filter_3d(v, r, iterations);
+        for (int z = 0; z < d; ++z)
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x)
+                    out[(static_cast<size_t>(z) * h + y) * w + x] = res(x, y, z);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// SummedVolumeTable (integral.hpp:98-113): cumsum((w+1)x(h+1)x(d+1))
+int ref_svt(const double* in, int w, int h, int d, double* cumsum) {
+    try {
+        const osbf::SummedVolumeTable t(to_volume(in, w, h, d));
+        for (int z = 0; z <= d; ++z)
+            for (int y = 0; y <= h; ++y)
+                for (int x = 0; x <= w; ++x)
+                    cumsum[(static_cast<size_t>(z) * (h + 1) + y) * (w + 1) + x] = t.cumsum(x, y, z);
         return 0;
     } catch (...) {
         return map_exception();

@@ -18,12 +18,14 @@ from .api import (  # noqa: F401
     OutOfRange,
     SubWindowId,
     box_filter,
+    box_filter_3d,
     build_sat,
     default_context,
     fast_osbf,
     filter_multichannel,
     max_threads,
     osbf,
+    osbf_3d,
     osbf_step,
     set_max_threads,
     sub_windows,
@@ -32,6 +34,7 @@ from .api import (  # noqa: F401
 
 __all__ = [
     "build", "lib", "Context", "default_context", "osbf", "osbf_step", "fast_osbf", "box_filter",
+    "osbf_3d", "box_filter_3d",
     "filter_multichannel",
     "build_sat", "subwindow_means", "sub_windows", "SubWindowId", "FilterConfig", "FilterVariant",
     "set_max_threads", "max_threads", "OsbfError", "InvalidArgument", "DomainError", "OutOfRange",

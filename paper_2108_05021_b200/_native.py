@@ -47,6 +47,10 @@ SIGNATURES = [
     ("osbf_gpu_box_filter", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_void_p, _c_size, _c_size,
       _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),
+    ("osbf_gpu_osbf_3d", _c_int,
+     [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),
+    ("osbf_gpu_box_filter_3d", _c_int,
+     [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_void_p]),
     ("osbf_gpu_subwindow_means", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_size, _c_size, _c_int, _c_int, _c_int, _c_int,
       _c_void_p, _c_void_p, _c_int, _c_void_p]),
@@ -68,6 +72,10 @@ SIGNATURES = [
       _c_int, _c_int, _c_int]),
     ("osbf_gpu_fast_osbf_host", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
+    ("osbf_gpu_osbf_3d_host", _c_int,
+     [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
+    ("osbf_gpu_box_filter_3d_host", _c_int,
+     [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
     ("osbf_gpu_box_filter_host", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
     ("osbf_gpu_filter_multichannel_box_host", _c_int,

@@ -17,6 +17,8 @@ reference                              here
 ``osbf`` filters2d.hpp:91              :func:`osbf`
 ``fast_osbf`` filters2d.hpp:105        :func:`fast_osbf` (paper Algorithm 3, bit-identical)
 ``box_filter`` filters2d.hpp:38        :func:`box_filter` (bit-identical)
+``osbf_3d`` / ``box_filter_3d``        :func:`osbf_3d` / :func:`box_filter_3d` (bit-identical)
+ filters3d.hpp:55-114
 ``filter_multichannel`` :371           :func:`filter_multichannel` (OsbfExact, OsbfFast, Box)
 ``set_max_threads`` parallel.hpp:20    :func:`set_max_threads` (no-op: the GPU
                                         result does not depend on any launch knob)
@@ -213,6 +215,40 @@ class Context:
         """The classical box filter (filters2d.hpp:38-56) over a CUDA tensor;
         bit-identical to the reference's box_filter."""
         return self._sat_filter("osbf_gpu_box_filter", src, radius, iterations, out, stream)
+
+    def osbf_3d(self, vol, radius: int, iterations: int, out=None, stream=None):
+        """filters3d.hpp:78-114 on a CUDA float64 volume (D, H, W); bit-identical."""
+        return self._filter3d("osbf_gpu_osbf_3d", vol, radius, iterations, out, stream)
+
+    def box_filter_3d(self, vol, radius: int, iterations: int, out=None, stream=None):
+        """filters3d.hpp:55-76 on a CUDA float64 volume (D, H, W); bit-identical."""
+        return self._filter3d("osbf_gpu_box_filter_3d", vol, radius, iterations, out, stream)
+
+    def _filter3d(self, fn, vol, radius, iterations, out, stream):
+        import torch
+
+        if vol.dim() != 3 or vol.dtype != torch.float64 or not vol.is_contiguous():
+            raise InvalidArgument("expected a contiguous float64 (D, H, W) volume")
+        d, h, w = vol.shape
+        if out is None:
+            out = torch.empty_like(vol)
+        if stream is None:
+            stream = torch.cuda.current_stream(vol.device).cuda_stream
+        _check(getattr(self._lib, fn)(self.handle, ctypes.c_void_p(vol.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr()), w, h, d, radius,
+                                      iterations, ctypes.c_void_p(stream)))
+        return out
+
+    def filter3d_host(self, vol: np.ndarray, radius: int, iterations: int, osbf3=True):
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        if v.ndim != 3:
+            raise InvalidArgument("expected a (D, H, W) volume")
+        d, h, w = v.shape
+        out = np.empty_like(v)
+        fn = self._lib.osbf_gpu_osbf_3d_host if osbf3 else self._lib.osbf_gpu_box_filter_3d_host
+        _check(fn(self.handle, ctypes.c_void_p(v.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                  w, h, d, radius, iterations))
+        return out
 
     def _sat_filter(self, fn, src, radius, iterations, out, stream):
         import torch
@@ -464,6 +500,21 @@ def box_filter(plane, r: int, iterations: int):
     if _is_tensor(plane):
         return default_context(plane.device.index or 0).box_filter(plane, r, iterations)
     return default_context().box_filter_host(np.asarray(plane), r, iterations)
+
+
+def osbf_3d(vol, r: int, iterations: int):
+    """filters3d.hpp:78-114 — 14 one-sided regions, bit-identical; numpy or
+    CUDA float64 volume of shape (D, H, W)."""
+    if _is_tensor(vol):
+        return default_context(vol.device.index or 0).osbf_3d(vol, r, iterations)
+    return default_context().filter3d_host(np.asarray(vol), r, iterations, osbf3=True)
+
+
+def box_filter_3d(vol, r: int, iterations: int):
+    """filters3d.hpp:55-76 — bit-identical; numpy or CUDA float64 (D, H, W)."""
+    if _is_tensor(vol):
+        return default_context(vol.device.index or 0).box_filter_3d(vol, r, iterations)
+    return default_context().filter3d_host(np.asarray(vol), r, iterations, osbf3=False)
 
 
 def filter_multichannel(channels, config: FilterConfig, mode="exact"):

@@ -562,6 +562,105 @@ osbf_status osbf_gpu_box_filter(osbf_ctx* ctx, osbf_dtype in_dtype, const void* 
                       stream);
 }
 
+}  // extern "C"
+
+namespace {
+// osbf_3d / box_filter_3d (filters3d.hpp:55-114) on one fp64 volume [D][H][W].
+osbf_status filter3d(osbf_ctx* ctx, bool osbf3, const double* d_in, double* d_out, int width,
+                     int height, int depth, int radius, int iterations, void* stream) {
+    const char* name = osbf3 ? "osbf_3d" : "box_filter_3d";
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "%s: radius must be >= 1", name);
+    if (iterations < 0)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "%s: iterations must be >= 0", name);
+    if (width < 1 || height < 1 || depth < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "Volume: extents must be >= 1");
+    if (!d_in || !d_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null volume pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = pick_stream(ctx, stream);
+    const size_t n = static_cast<size_t>(width) * height * depth;
+    // the volume as a width x (height*depth) plane for the ping-pong logic
+    const osbf_gpu::Geometry g{width, height * depth, 1};
+    const osbf_gpu::PlaneView input{d_in, OSBF_F64, static_cast<size_t>(width), n};
+    if (iterations == 0) {
+        if (d_out != d_in)
+            OSBF_CUDA(cudaMemcpyAsync(d_out, d_in, n * sizeof(double), cudaMemcpyDeviceToDevice, s),
+                      "copy");
+        return OSBF_OK;
+    }
+    OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc rows");
+    OSBF_CUDA(ctx->sat.ensure(osbf_gpu::svt_elems(width, height, depth) * sizeof(double)),
+              "alloc table");
+    auto body = [&](cudaStream_t st_) {
+        return jacobi(
+            ctx, input, g, iterations, d_out, static_cast<size_t>(width), n, st_,
+            [](int) { return 1; },
+            [&](const osbf_gpu::PlaneView& src, double* dst, size_t, size_t, int,
+                bool*) -> osbf_status {
+                OSBF_CUDA(osbf_gpu::filter3d_pass(static_cast<const double*>(src.base), width,
+                                                  height, depth, radius, osbf3,
+                                                  ctx->rowpfx.as<double>(), ctx->sat.as<double>(),
+                                                  dst, st_, ctx->lc),
+                          name);
+                return OSBF_OK;
+            });
+    };
+    const std::vector<uintptr_t> key = {
+        osbf3 ? 5u : 4u, reinterpret_cast<uintptr_t>(d_in), reinterpret_cast<uintptr_t>(d_out),
+        static_cast<uintptr_t>(width), static_cast<uintptr_t>(height),
+        static_cast<uintptr_t>(depth), static_cast<uintptr_t>(radius),
+        static_cast<uintptr_t>(iterations)};
+    return run_graphed(ctx, key, s, body);
+}
+
+osbf_status filter3d_host(osbf_ctx* ctx, bool osbf3, const double* h_in, double* h_out, int width,
+                          int height, int depth, int radius, int iterations) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (!h_in || !h_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    if (width < 1 || height < 1 || depth < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "Volume: extents must be >= 1");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t n = static_cast<size_t>(width) * height * depth;
+    OSBF_CUDA(ctx->host_in.ensure(n * sizeof(double)), "alloc input");
+    OSBF_CUDA(ctx->host_out.ensure(n * sizeof(double)), "alloc output");
+    cudaStream_t s = ctx->stream;
+    OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * sizeof(double), cudaMemcpyHostToDevice, s),
+              "H2D");
+    osbf_status st = filter3d(ctx, osbf3, ctx->host_in.as<double>(), ctx->host_out.as<double>(),
+                              width, height, depth, radius, iterations, s);
+    if (st != OSBF_OK) return st;
+    OSBF_CUDA(cudaMemcpyAsync(h_out, ctx->host_out.ptr, n * sizeof(double), cudaMemcpyDeviceToHost,
+                              s),
+              "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+osbf_status osbf_gpu_osbf_3d(osbf_ctx* ctx, const double* d_in, double* d_out, int width,
+                            int height, int depth, int radius, int iterations, void* stream) {
+    return filter3d(ctx, true, d_in, d_out, width, height, depth, radius, iterations, stream);
+}
+
+osbf_status osbf_gpu_box_filter_3d(osbf_ctx* ctx, const double* d_in, double* d_out, int width,
+                                  int height, int depth, int radius, int iterations,
+                                  void* stream) {
+    return filter3d(ctx, false, d_in, d_out, width, height, depth, radius, iterations, stream);
+}
+
+osbf_status osbf_gpu_osbf_3d_host(osbf_ctx* ctx, const double* h_in, double* h_out, int width,
+                                 int height, int depth, int radius, int iterations) {
+    return filter3d_host(ctx, true, h_in, h_out, width, height, depth, radius, iterations);
+}
+
+osbf_status osbf_gpu_box_filter_3d_host(osbf_ctx* ctx, const double* h_in, double* h_out,
+                                       int width, int height, int depth, int radius,
+                                       int iterations) {
+    return filter3d_host(ctx, false, h_in, h_out, width, height, depth, radius, iterations);
+}
+
 osbf_status osbf_gpu_subwindow_means(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_in,
                                      size_t in_pitch, size_t in_plane_stride, int width,
                                      int height, int batch, int radius, double* d_means,

@@ -102,6 +102,14 @@ cudaError_t boxfilter_pass(const PlaneView& in, const Geometry& g, int radius, d
                            double* sat, double* out, size_t out_pitch, size_t out_plane,
                            cudaStream_t s, LaunchCounter& lc);
 
+// ---- 3-D extension (osbf_3d.cu) -------------------------------------------
+// One osbf_3d / box_filter_3d iteration on an fp64 volume [D][H][W]:
+// rowp W*H*D and table svt_elems(W, H, D) doubles of workspace.
+size_t svt_elems(int W, int H, int D);
+cudaError_t filter3d_pass(const double* in, int W, int H, int D, int r, bool osbf,
+                          double* rowp, double* table, double* out, cudaStream_t s,
+                          LaunchCounter& lc);
+
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
 // Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
 constexpr int kFastMaxRadius = 16;

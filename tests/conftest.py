@@ -54,6 +54,10 @@ def boxfilter_golden_cases():
     return sorted(glob.glob(os.path.join(GOLDEN_DIR, "boxfilter", "*.npz")))
 
 
+def filter3d_golden_cases():
+    return sorted(glob.glob(os.path.join(GOLDEN_DIR, "filters3d", "*.npz")))
+
+
 def load_golden(path):
     d = np.load(path)
     return {k: d[k] for k in d.files}

@@ -118,6 +118,21 @@ def box_filter_cases():
     return out
 
 
+def filter3d_cases():
+    """(name, volume (D, H, W), r, iterations, osbf3) for filters3d.hpp."""
+    out = []
+    rng = np.random.default_rng(36)
+    for r in (1, 2, 3):
+        out.append((f"osbf3d_random_9x10x12_r{r}", rng.random((9, 10, 12)) * 255, r, 2, True))
+    step = np.where(np.arange(16)[None, None, :] < 8, 10.0, 90.0) * np.ones((8, 6, 1))
+    out.append(("osbf3d_step_8x6x16_r2", step, 2, 1, True))  # test_filters3d.cpp:80-100
+    out.append(("osbf3d_ragged_5x1x7_r2", rng.random((5, 1, 7)), 2, 3, True))
+    for r in (1, 3):
+        out.append((f"box3d_random_7x9x11_r{r}", rng.random((7, 9, 11)) * 100, r, 2, False))
+    out.append(("box3d_constant_r2", np.full((4, 5, 6), 2.5), 2, 3, False))
+    return out
+
+
 def main() -> None:
     ref = Reference()
     ref.set_max_threads(1)
@@ -148,6 +163,13 @@ def main() -> None:
         np.savez_compressed(os.path.join(HERE, "boxfilter", f"{name}.npz"), input=inp,
                             output=out, radius=r, iterations=iters)
         print(f"boxfilter/{name:20s} in {inp.shape} {inp.dtype} r={r} it={iters}")
+    os.makedirs(os.path.join(HERE, "filters3d"), exist_ok=True)
+    for name, vol, r, iters, osbf3 in filter3d_cases():
+        out = ref.osbf_3d(vol, r, iters) if osbf3 else ref.box_filter_3d(vol, r, iters)
+        np.savez_compressed(os.path.join(HERE, "filters3d", f"{name}.npz"), input=vol,
+                            output=out, radius=r, iterations=iters, osbf3=osbf3,
+                            svt=ref.svt(vol))
+        print(f"filters3d/{name:28s} {vol.shape} r={r} it={iters}")
     # integral.hpp / test_integral.cpp:19-29 known SAT
     p = np.array([[1.0, 2.0], [3.0, 4.0]])
     np.savez_compressed(os.path.join(HERE, "sat_2x2.npz"), input=p, cumsum=ref.sat(p))
