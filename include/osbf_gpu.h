@@ -233,6 +233,11 @@ osbf_status osbf_gpu_box_filter_3d_host(osbf_ctx* ctx, const double* h_in, doubl
                                        int width, int height, int depth, int radius,
                                        int iterations);
 
+/* SummedVolumeTable (integral.hpp:98-113) built on the GPU, bit-identical:
+ * h_cumsum receives (width+1)*(height+1)*(depth+1) doubles, x fastest. */
+osbf_status osbf_gpu_svt_host(osbf_ctx* ctx, const double* h_in, int width, int height, int depth,
+                             double* h_cumsum);
+
 /* osbf::box_filter on host memory (batch planes back to back). */
 osbf_status osbf_gpu_box_filter_host(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in,
                                      double* h_out, int width, int height, int batch, int radius,

@@ -250,6 +250,18 @@ class Context:
                   w, h, d, radius, iterations))
         return out
 
+    def svt_host(self, vol: np.ndarray) -> np.ndarray:
+        """Summed-volume table (integral.hpp:98-112 order) of a (D, H, W) host
+        volume, built on the GPU; shape (D+1, H+1, W+1) with zero border slabs."""
+        v = np.ascontiguousarray(vol, dtype=np.float64)
+        if v.ndim != 3:
+            raise InvalidArgument("expected a (D, H, W) volume")
+        d, h, w = v.shape
+        out = np.empty((d + 1, h + 1, w + 1), dtype=np.float64)
+        _check(self._lib.osbf_gpu_svt_host(self.handle, ctypes.c_void_p(v.ctypes.data), w, h, d,
+                                           ctypes.c_void_p(out.ctypes.data)))
+        return out
+
     def _sat_filter(self, fn, src, radius, iterations, out, stream):
         import torch
 

@@ -113,21 +113,29 @@ size_t svt_elems(int W, int H, int D) {
     return (static_cast<size_t>(W) + 1) * (static_cast<size_t>(H) + 1) * (static_cast<size_t>(D) + 1);
 }
 
-cudaError_t filter3d_pass(const double* in, int W, int H, int D, int r, bool osbf,
-                          double* rowp, double* table, double* out, cudaStream_t s,
-                          LaunchCounter& lc) {
+cudaError_t svt_build(const double* in, int W, int H, int D, double* rowp, double* table,
+                      cudaStream_t s, LaunchCounter& lc) {
     const long long rows = static_cast<long long>(H) * D;
     cudaError_t e = cudaMemsetAsync(table, 0, sizeof(double) * svt_elems(W, H, D), s);
     if (e != cudaSuccess) return e;
     svt_rows<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, s>>>(in, rowp, W, rows);
     svt_columns<<<(W + 127) / 128, 128, 0, s>>>(rowp, table, W, H, D);
+    lc.launches += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t filter3d_pass(const double* in, int W, int H, int D, int r, bool osbf,
+                          double* rowp, double* table, double* out, cudaStream_t s,
+                          LaunchCounter& lc) {
+    cudaError_t e = svt_build(in, W, H, D, rowp, table, s, lc);
+    if (e != cudaSuccess) return e;
     const long long n = static_cast<long long>(W) * H * D;
     const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
     if (osbf)
         filter3d<true><<<blocks, 256, 0, s>>>(in, table, out, W, H, D, r);
     else
         filter3d<false><<<blocks, 256, 0, s>>>(in, table, out, W, H, D, r);
-    lc.launches += 3;
+    lc.launches += 1;
     return cudaGetLastError();
 }
 

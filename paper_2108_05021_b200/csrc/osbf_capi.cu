@@ -655,6 +655,31 @@ osbf_status osbf_gpu_osbf_3d_host(osbf_ctx* ctx, const double* h_in, double* h_o
     return filter3d_host(ctx, true, h_in, h_out, width, height, depth, radius, iterations);
 }
 
+osbf_status osbf_gpu_svt_host(osbf_ctx* ctx, const double* h_in, int width, int height, int depth,
+                             double* h_cumsum) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    if (!h_in || !h_cumsum) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    if (width < 1 || height < 1 || depth < 1)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "Volume: extents must be >= 1");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t n = static_cast<size_t>(width) * height * depth;
+    const size_t nt = osbf_gpu::svt_elems(width, height, depth);
+    OSBF_CUDA(ctx->host_in.ensure(n * sizeof(double)), "alloc input");
+    OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc rows");
+    OSBF_CUDA(ctx->host_out.ensure(nt * sizeof(double)), "alloc table");
+    cudaStream_t s = ctx->stream;
+    OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * sizeof(double), cudaMemcpyHostToDevice, s),
+              "H2D");
+    OSBF_CUDA(osbf_gpu::svt_build(ctx->host_in.as<double>(), width, height, depth,
+                                  ctx->rowpfx.as<double>(), ctx->host_out.as<double>(), s, ctx->lc),
+              "svt");
+    OSBF_CUDA(cudaMemcpyAsync(h_cumsum, ctx->host_out.ptr, nt * sizeof(double),
+                              cudaMemcpyDeviceToHost, s),
+              "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+
 osbf_status osbf_gpu_box_filter_3d_host(osbf_ctx* ctx, const double* h_in, double* h_out,
                                        int width, int height, int depth, int radius,
                                        int iterations) {

@@ -106,6 +106,8 @@ cudaError_t boxfilter_pass(const PlaneView& in, const Geometry& g, int radius, d
 // One osbf_3d / box_filter_3d iteration on an fp64 volume [D][H][W]:
 // rowp W*H*D and table svt_elems(W, H, D) doubles of workspace.
 size_t svt_elems(int W, int H, int D);
+cudaError_t svt_build(const double* in, int W, int H, int D, double* rowp, double* table,
+                      cudaStream_t s, LaunchCounter& lc);
 cudaError_t filter3d_pass(const double* in, int W, int H, int D, int r, bool osbf,
                           double* rowp, double* table, double* out, cudaStream_t s,
                           LaunchCounter& lc);

@@ -1,9 +1,11 @@
 // C++ drop-in test: the reference's hot-path test cases (proj/tests/
-// test_core.cpp, test_integral.cpp, test_filters2d.cpp, acceptance.cpp
+// test_core.cpp, test_integral.cpp, test_filters2d.cpp, test_filters3d.cpp,
+// acceptance.cpp
 // criteria 1, 2, 5) re-expressed against include/osbf/*.hpp, which run on the
 // GPU through libosbf_gpu.so.  The CPU checker is the oracle restatement
 // (oracle/osbf_oracle.c; test infrastructure only).  Prints one PASS/FAIL
 // line per case; exit code = number of failures.
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -86,6 +88,24 @@ ImagePlane checker_osbf(const ImagePlane& p, int r, int it) {
     if (oracle_osbf(p.samples().data(), out.samples().data(), p.width(), p.height(), r, it) != 0)
         throw std::runtime_error("oracle failed");
     return out;
+}
+
+osbf::Volume random_volume(int w, int h, int d, std::uint64_t seed, double lo = 0.0,
+                           double hi = 255.0) {
+    osbf::Volume v(w, h, d);
+    std::mt19937_64 rng(seed);
+    for (double& s : v.samples()) s = lo + (hi - lo) * (static_cast<double>(rng() >> 11) * 0x1.0p-53);
+    return v;
+}
+
+bool bit_equal(const osbf::Volume& a, const std::vector<double>& b) {
+    return a.size() == b.size() && std::memcmp(a.samples().data(), b.data(), b.size() * sizeof(double)) == 0;
+}
+
+double max_abs_diff(const osbf::Volume& a, const osbf::Volume& b) {
+    double m = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.samples()[i] - b.samples()[i]));
+    return m;
 }
 
 }  // namespace
@@ -331,6 +351,93 @@ int main() {
                 if (!bit_equal(osbf::osbf(p, r, 3), checker_osbf(p, r, 3))) return false;
         }
         return true;
+    });
+
+    // ---- 3-D extension: test_core.cpp:73-78, test_integral.cpp:101-129,
+    //      test_filters3d.cpp:32-117
+    run("Volume extents, accessors and errors", [] {
+        osbf::Volume v(2, 3, 2, 0.0);
+        v.set(1, 2, 1, 5.0);
+        return v.size() == 12 && v(1, 2, 1) == 5.0 && v.get(1, 2, 1) == 5.0 &&
+               v.samples()[(1 * 3 + 2) * 2 + 1] == 5.0 &&
+               throws<std::out_of_range>([&] { v.get(2, 0, 0); }) &&
+               throws<std::invalid_argument>([] { osbf::Volume(0, 1, 1); }) &&
+               throws<std::invalid_argument>([] { osbf::Volume(2, 2, 2, std::vector<double>(7)); });
+    });
+    run("SummedVolumeTable (GPU-built) bit-identical to the oracle; box lookups", [] {
+        const auto ones = osbf::build_svt(osbf::Volume(4, 4, 4, 1.0));
+        if (osbf::box_sum_3d(ones, {0, 0, 0, 3, 3, 3}) != 64.0 ||
+            osbf::box_sum_3d(ones, {-5, -5, -5, 10, 10, 10}) != 64.0)
+            return false;
+        osbf::Volume v(3, 3, 3, 0.0);
+        v(1, 2, 1) = 42.0;
+        const auto sv = osbf::build_svt(v);
+        if (osbf::box_sum_3d(sv, {1, 2, 1, 1, 2, 1}) != 42.0 ||
+            osbf::box_mean_3d(sv, {1, 2, 1, 1, 2, 1}) != 42.0)
+            return false;
+        if (!throws<std::domain_error>([&] { osbf::box_mean_3d(sv, {5, 5, 5, 9, 9, 9}); })) return false;
+        const std::array<std::array<int, 3>, 3> shapes{{{8, 8, 8}, {13, 5, 9}, {1, 17, 3}}};
+        for (const auto& [w, h, d] : shapes) {
+            const auto rv = random_volume(w, h, d, 61 + w);
+            std::vector<double> want(static_cast<size_t>(w + 1) * (h + 1) * (d + 1));
+            oracle_svt_build(rv.samples().data(), w, h, d, want.data());
+            const osbf::SummedVolumeTable svt(rv);
+            for (int z = 0; z <= d; ++z)
+                for (int y = 0; y <= h; ++y)
+                    for (int x = 0; x <= w; ++x) {
+                        const double g = svt.cumsum(x, y, z);
+                        const double e = want[(static_cast<size_t>(z) * (h + 1) + y) * (w + 1) + x];
+                        if (std::memcmp(&g, &e, sizeof(double)) != 0) return false;
+                    }
+        }
+        return true;
+    });
+    run("sub_regions_3d: ids, one-sided extents, voxel counts", [] {
+        const int r = 2;
+        const auto regions = osbf::sub_regions_3d(r);
+        for (int i = 0; i < 14; ++i) {
+            const auto& g = regions[static_cast<size_t>(i)];
+            if (g.id != i + 1 || g.u0 > 0 || g.u1 < 0 || g.v0 > 0 || g.v1 < 0 || g.w0 > 0 || g.w1 < 0)
+                return false;
+            const long long n = static_cast<long long>(g.u1 - g.u0 + 1) * (g.v1 - g.v0 + 1) * (g.w1 - g.w0 + 1);
+            if (n != (i < 8 ? 27LL : 75LL)) return false;
+        }
+        return throws<std::invalid_argument>([] { osbf::sub_regions_3d(0); });
+    });
+    run("box_filter_3d / osbf_3d bit-identical to the oracle; fixed points; errors", [] {
+        const osbf::Volume c(6, 6, 6, 4.0);
+        if (max_abs_diff(osbf::box_filter_3d(c, 2, 3), c) != 0.0 ||
+            max_abs_diff(osbf::osbf_3d(c, 2, 2), c) != 0.0)
+            return false;
+        for (int r : {1, 2, 3}) {
+            const auto v = random_volume(11, 9, 7, 62 + r);
+            std::vector<double> want(v.size());
+            if (oracle_box_filter_3d(v.samples().data(), want.data(), 11, 9, 7, r, 2) != 0 ||
+                !bit_equal(osbf::box_filter_3d(v, r, 2), want))
+                return false;
+            if (oracle_osbf_3d(v.samples().data(), want.data(), 11, 9, 7, r, 2) != 0 ||
+                !bit_equal(osbf::osbf_3d(v, r, 2), want))
+                return false;
+        }
+        // axis steps stay fixed (test_filters3d.cpp:80-100)
+        osbf::Volume sx(16, 8, 8, 0.0), sy(8, 16, 8, 0.0), sz(8, 8, 16, 0.0);
+        for (int z = 0; z < 8; ++z)
+            for (int y = 0; y < 8; ++y)
+                for (int x = 0; x < 16; ++x) {
+                    sx(x, y, z) = x < 8 ? 0.0 : 100.0;
+                    sy(y, x, z) = x < 8 ? 0.0 : 100.0;
+                    sz(y, z, x) = x < 8 ? 0.0 : 100.0;
+                }
+        const std::array<const osbf::Volume*, 3> steps{&sx, &sy, &sz};
+        for (const auto* s : steps)
+            if (max_abs_diff(osbf::osbf_3d(*s, 2, 1), *s) != 0.0) return false;
+        const auto v = random_volume(10, 10, 10, 63, 5.0, 50.0);
+        const auto filtered = osbf::osbf_3d(v, 2, 3);
+        for (double s : filtered.samples())
+            if (s < 5.0 || s > 50.0) return false;
+        return max_abs_diff(osbf::osbf_3d(v, 2, 0), v) == 0.0 &&
+               throws<std::invalid_argument>([&] { osbf::osbf_3d(v, 0, 1); }) &&
+               throws<std::invalid_argument>([&] { osbf::box_filter_3d(v, 1, -1); });
     });
 
     std::printf("%d failure(s)\n", failures);

@@ -53,6 +53,8 @@ def test_3d_gpu_matches_reference_golden(ctx, path):
     got = (ctx.osbf_3d(dv, r, it) if osbf3 else ctx.box_filter_3d(dv, r, it)).cpu().numpy()
     assert np.array_equal(bits(got), bits(g["output"]))
     assert np.array_equal(bits(ctx.filter3d_host(v, r, it, osbf3=osbf3)), bits(g["output"]))
+    svt = ctx.svt_host(v)
+    assert np.array_equal(bits(svt.reshape(-1)), bits(np.asarray(g["svt"]).reshape(-1)))
 
 
 @pytest.mark.gpu
@@ -68,6 +70,7 @@ def test_3d_gpu_random_and_errors(ctx, oracle_lib):
         assert np.array_equal(bits(got), bits(oracle_lib.osbf_3d(v, r, 2)))
         got = ctx.box_filter_3d(torch.from_numpy(v).cuda(), r, 2).cpu().numpy()
         assert np.array_equal(bits(got), bits(oracle_lib.box_filter_3d(v, r, 2)))
+        assert np.array_equal(bits(ctx.svt_host(v)), bits(oracle_lib.svt(v)))
     with pytest.raises(ob.InvalidArgument):
         ob.osbf_3d(np.ones((2, 2, 2)), 0, 0)
     with pytest.raises(ob.InvalidArgument):

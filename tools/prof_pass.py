@@ -1,6 +1,8 @@
 """Quick per-pass timing of the OSBF kernels (CUDA events, warm, L2-flushed).
-usage: python tools/prof_pass.py [--mode fast|exact|fastosbf] [--radii 1,2,4,8,16] [--shape B,H,W]
-(fastosbf = paper Algorithm 3, osbf_gpu_fast_osbf)"""
+usage: python tools/prof_pass.py [--mode fast|exact|fastosbf|box|osbf3d|box3d] [--radii 1,2,4,8,16]
+                                 [--shape B,H,W]
+(fastosbf = paper Algorithm 3, osbf_gpu_fast_osbf; box = osbf_gpu_box_filter;
+ osbf3d / box3d = the 3-D filters with --shape read as D,H,W)"""
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -19,8 +21,11 @@ y = torch.empty_like(x)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 for r in map(int, a.radii.split(",")):
-    run = ((lambda: ctx.fast_osbf(x, r, 1, out=y)) if a.mode == "fastosbf"
-           else (lambda: ctx.iterate(x, r, 1, mode=a.mode, out=y)))
+    run = {"fastosbf": lambda: ctx.fast_osbf(x, r, 1, out=y),
+           "box": lambda: ctx.box_filter(x, r, 1, out=y),
+           "osbf3d": lambda: ctx.osbf_3d(x, r, 1, out=y),
+           "box3d": lambda: ctx.box_filter_3d(x, r, 1, out=y)}.get(
+               a.mode, lambda: ctx.iterate(x, r, 1, mode=a.mode, out=y))
     for _ in range(3):
         run()
     ts = []
