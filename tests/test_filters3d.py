@@ -75,3 +75,15 @@ def test_3d_gpu_random_and_errors(ctx, oracle_lib):
         ob.osbf_3d(np.ones((2, 2, 2)), 0, 0)
     with pytest.raises(ob.InvalidArgument):
         ob.box_filter_3d(np.ones((2, 2, 2)), 1, -1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(300, 200, 5), (260, 128, 3), (257, 129, 9), (140, 133, 4),
+                                   (129, 1, 7), (1, 300, 2), (2, 2, 37), (513, 7, 1)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_svt_wavefront_regimes_bit_exact(ctx, oracle_lib, shape):
+    """osbf_3d.cu svt_yz: plane slots restart every Hp steps (H below, at and
+    just above the 128 slots; several wraps over z) — bit-identical tables."""
+    rng = np.random.default_rng(sum(shape))
+    v = rng.random(shape) * 255
+    assert np.array_equal(bits(ctx.svt_host(v)), bits(oracle_lib.svt(v)))
