@@ -254,6 +254,27 @@ osbf_status osbf_gpu_filter_multichannel_fast_host(osbf_ctx* ctx, const double* 
                                                    double* const* h_out, int channels, int width,
                                                    int height, int radius, int iterations);
 
+/* The `osbf smooth` edge (tools/osbf_main.cpp:63-83):
+ * read_image's promotion (io.hpp:122-178), filter_multichannel with the
+ * given filter and write_image's quantisation (io.hpp:187-215: round half
+ * up, negatives/NaN to 0, clamp to 255 or 65535, quantize io.hpp:108-115)
+ * in one call.  `h_raster` holds the decoded, host-endian samples of a
+ * PGM/PPM payload, interleaved (channels 1 or 3, sample_bytes 1 = uint8,
+ * 2 = uint16); `h_out` receives the quantised interleaved samples
+ * (out_sample_bytes 1 -> maxval 255, 2 -> 65535).  Promotion and
+ * quantisation run on the GPU, so the raster crosses PCIe as 1-2 B per
+ * sample.  `mode` applies to OSBF_FILTER_OSBF only. */
+typedef enum osbf_filter {
+    OSBF_FILTER_OSBF = 0,      /* FilterVariant::OsbfExact, CLI "osbf"       */
+    OSBF_FILTER_FAST_OSBF = 1, /* FilterVariant::OsbfFast,  CLI "fast-osbf"  */
+    OSBF_FILTER_BOX = 2        /* FilterVariant::Box,       CLI "box"        */
+} osbf_filter;
+
+osbf_status osbf_gpu_smooth_raster_host(osbf_ctx* ctx, const void* h_raster, int sample_bytes,
+                                        int channels, int width, int height, osbf_filter filter,
+                                        int radius, int iterations, osbf_mode mode, void* h_out,
+                                        int out_sample_bytes);
+
 /* SummedAreaTable construction (integral.hpp:16-30) for host planes. */
 osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,
                               double* h_cumsum);

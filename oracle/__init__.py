@@ -71,6 +71,9 @@ class Oracle:
         lib.oracle_svt_build.restype = None
         lib.oracle_osbf_3d.argtypes = [_dp, _dp] + [ctypes.c_int] * 5
         lib.oracle_box_filter_3d.argtypes = lib.oracle_osbf_3d.argtypes
+        lib.oracle_quantize.argtypes = [ctypes.c_double, ctypes.c_int]
+        lib.oracle_smooth_raster.argtypes = ([ctypes.c_void_p] + [ctypes.c_int] * 7 +
+                                             [ctypes.c_void_p, ctypes.c_int])
         self.lib = lib
 
     def sub_windows(self, r: int):
@@ -110,6 +113,24 @@ class Oracle:
         st = fn(_ptr(v), _ptr(out), w, h, d, r, iterations)
         if st:
             raise CheckerError(st, name)
+        return out
+
+    def quantize(self, v: float, maxval: int) -> int:
+        """io.hpp:108-115."""
+        return self.lib.oracle_quantize(v, maxval)
+
+    def smooth_raster(self, raster, filter: str, r: int, iterations: int,
+                      out_bits: int = 8) -> np.ndarray:
+        """tools/osbf_main.cpp:63-83 without file I/O: promote, filter, quantise."""
+        x = np.ascontiguousarray(raster)
+        h, w = x.shape[:2]
+        c = 1 if x.ndim == 2 else x.shape[2]
+        out = np.empty(x.shape, dtype=np.uint8 if out_bits == 8 else np.uint16)
+        st = self.lib.oracle_smooth_raster(x.ctypes.data, x.dtype.itemsize, c, w, h,
+                                           SMOOTH_FILTERS[filter], r, iterations, out.ctypes.data,
+                                           out.dtype.itemsize)
+        if st:
+            raise CheckerError(st, "smooth_raster")
         return out
 
     def box_filter(self, plane, r: int, iterations: int) -> np.ndarray:
@@ -183,6 +204,8 @@ class Reference:
         lib.ref_sat.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
         lib.ref_subwindow_means.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _u8p]
         lib.ref_rect_mean.argtypes = [_dp] + [ctypes.c_int] * 6 + [_dp]
+        lib.ref_quantize.argtypes = [ctypes.c_double, ctypes.c_int]
+        lib.ref_smooth_file.argtypes = [ctypes.c_char_p, ctypes.c_char_p] + [ctypes.c_int] * 3
         lib.ref_set_max_threads.argtypes = [ctypes.c_int]
         lib.ref_set_max_threads.restype = None
         lib.ref_pin_allocator_for_timing.restype = None
@@ -300,3 +323,61 @@ class Reference:
         if st:
             raise CheckerError(st, "ref rect_mean")
         return m.value
+
+    def quantize(self, v: float, maxval: int) -> int:
+        return self.lib.ref_quantize(v, maxval)
+
+    def smooth_file(self, in_path: str, out_path: str, filter: str, r: int,
+                    iterations: int) -> None:
+        """cmd_smooth (tools/osbf_main.cpp:63-83) through the reference's own
+        read_image / filter_multichannel / write_image."""
+        st = self.lib.ref_smooth_file(in_path.encode(), out_path.encode(), SMOOTH_FILTERS[filter],
+                                      r, iterations)
+        if st:
+            raise CheckerError(st, "ref smooth_file")
+
+    def smooth_raster(self, raster, filter: str, r: int, iterations: int, tmpdir: str,
+                      maxval: int | None = None) -> np.ndarray:
+        """smooth_file on a raster written as binary PGM/PPM (maxval defaults to
+        255 for uint8, 65535 for uint16), output read back."""
+        x = np.ascontiguousarray(raster)
+        if maxval is None:
+            maxval = 255 if x.dtype == np.uint8 else 65535
+        src = os.path.join(tmpdir, "ref_in.pnm")
+        dst = os.path.join(tmpdir, "ref_out.pnm")
+        write_pnm(src, x, maxval)
+        self.smooth_file(src, dst, filter, r, iterations)
+        return read_pnm(dst)[0]
+
+
+SMOOTH_FILTERS = {"osbf": 0, "fast-osbf": 1, "box": 2}
+
+
+def write_pnm(path: str, raster: np.ndarray, maxval: int) -> None:
+    """Binary P5 (H, W) / P6 (H, W, 3); 2-byte big-endian samples when maxval > 255."""
+    x = np.asarray(raster)
+    magic = b"P5" if x.ndim == 2 else b"P6"
+    h, w = x.shape[:2]
+    payload = x.astype(">u2" if maxval > 255 else np.uint8).tobytes()
+    with open(path, "wb") as f:
+        f.write(magic + b"\n%d %d\n%d\n" % (w, h, maxval) + payload)
+
+
+def read_pnm(path: str):
+    """Binary P5/P6 as written by write_image (io.hpp:187-215) -> (raster, maxval)."""
+    data = open(path, "rb").read()
+    fields, pos = [], 2
+    while len(fields) < 3:
+        while data[pos:pos + 1].isspace():
+            pos += 1
+        start = pos
+        while not data[pos:pos + 1].isspace():
+            pos += 1
+        fields.append(int(data[start:pos]))
+    pos += 1
+    w, h, maxval = fields
+    c = 3 if data[:2] == b"P6" else 1
+    dt = np.dtype(">u2") if maxval > 255 else np.dtype(np.uint8)
+    x = np.frombuffer(data[pos:pos + w * h * c * dt.itemsize], dtype=dt)
+    x = x.astype(np.uint16 if maxval > 255 else np.uint8).reshape((h, w, c) if c == 3 else (h, w))
+    return x, maxval

@@ -11,6 +11,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -390,4 +391,51 @@ int oracle_box_filter_3d(const double* in, double* out, int w, int h, int d, int
 
 int oracle_osbf_3d(const double* in, double* out, int w, int h, int d, int r, int iters) {
     return filter3(in, out, w, h, d, r, iters, 1);
+}
+
+/* io.hpp:108-115 */
+int oracle_quantize(double v, int maxval) {
+    const double q = floor(v + 0.5);
+    if (!(q > 0.0)) return 0;
+    if (q > maxval) return maxval;
+    return (int)q;
+}
+
+/* tools/osbf_main.cpp:63-83 without the file I/O: read_image's promotion
+ * (io.hpp:157-168), FilterConfig::validate, filter_multichannel per channel,
+ * write_image's quantise + interleave (io.hpp:202-212). */
+int oracle_smooth_raster(const void* raster, int sample_bytes, int channels, int w, int h,
+                         int filter, int r, int iterations, void* out, int out_sample_bytes) {
+    if (r < 1 || iterations < 0 || (channels != 1 && channels != 3) || w < 1 || h < 1) return 1;
+    if ((sample_bytes != 1 && sample_bytes != 2) || (out_sample_bytes != 1 && out_sample_bytes != 2))
+        return 1;
+    if (filter < 0 || filter > 2) return 1;
+    const size_t n = (size_t)w * h;
+    double* plane = (double*)malloc(n * sizeof(double));
+    double* res = (double*)malloc(n * sizeof(double));
+    if (!plane || !res) {
+        free(plane);
+        free(res);
+        return 2;
+    }
+    const int maxval = out_sample_bytes == 1 ? 255 : 65535;
+    int st = 0;
+    for (int c = 0; c < channels && !st; ++c) {
+        for (size_t i = 0; i < n; ++i)
+            plane[i] = sample_bytes == 1 ? (double)((const uint8_t*)raster)[i * channels + c]
+                                         : (double)((const uint16_t*)raster)[i * channels + c];
+        st = filter == 1   ? oracle_fast_osbf(plane, res, w, h, r, iterations)
+             : filter == 2 ? oracle_box_filter(plane, res, w, h, r, iterations)
+                           : oracle_osbf(plane, res, w, h, r, iterations);
+        for (size_t i = 0; i < n && !st; ++i) {
+            const int q = oracle_quantize(res[i], maxval);
+            if (out_sample_bytes == 1)
+                ((uint8_t*)out)[i * channels + c] = (uint8_t)q;
+            else
+                ((uint16_t*)out)[i * channels + c] = (uint16_t)q;
+        }
+    }
+    free(plane);
+    free(res);
+    return st;
 }

@@ -80,6 +80,17 @@ void oracle_svt_build(const double* vol, int w, int h, int d, double* cumsum);
 int oracle_box_filter_3d(const double* in, double* out, int w, int h, int d, int r, int iters);
 int oracle_osbf_3d(const double* in, double* out, int w, int h, int d, int r, int iters);
 
+/* The `osbf smooth` edge (tools/osbf_main.cpp:63-83):
+ * io.hpp:108-115 quantize (floor(v + 0.5); negatives and NaN -> 0; clamp to
+ * maxval), and promote (io.hpp:157-168) -> filter_multichannel
+ * (filters2d.hpp:371-400; filter 0 osbf, 1 fast_osbf, 2 box) -> quantise +
+ * interleave (io.hpp:202-212) on an interleaved raster of uint8
+ * (sample_bytes 1) or uint16 (2) samples; out_sample_bytes 1 -> maxval 255,
+ * 2 -> 65535.  Returns nonzero on invalid arguments. */
+int oracle_quantize(double v, int maxval);
+int oracle_smooth_raster(const void* raster, int sample_bytes, int channels, int w, int h,
+                         int filter, int r, int iterations, void* out, int out_sample_bytes);
+
 #ifdef __cplusplus
 }
 #endif

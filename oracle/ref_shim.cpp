@@ -14,6 +14,7 @@
 #include "osbf/bench.hpp"
 #include "osbf/filters2d.hpp"
 #include "osbf/filters3d.hpp"
+#include "osbf/io.hpp"
 #include "osbf/parallel.hpp"
 
 namespace {
@@ -211,6 +212,32 @@ int ref_rect_mean(const double* in, int w, int h, int x0, int y0, int x1, int y1
     try {
         const auto sat = osbf::build_sat(to_plane(in, w, h));
         *mean = osbf::rect_mean(sat, x0, y0, x1, y1);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// osbf::detail::quantize (io.hpp:108-115)
+int ref_quantize(double v, int maxval) { return osbf::detail::quantize(v, maxval); }
+
+// tools/osbf_main.cpp:63-83 (cmd_smooth) through the reference's own file
+// I/O: read_image -> FilterConfig::validate -> filter_multichannel ->
+// write_image(bit depth 8 if maxval <= 255 else 16).  filter: 0 osbf,
+// 1 fast-osbf, 2 box.
+int ref_smooth_file(const char* in_path, const char* out_path, int filter, int r, int iterations) {
+    try {
+        int maxval = 255;
+        const osbf::MultiChannelImage img = osbf::read_image(in_path, &maxval);
+        osbf::FilterConfig cfg;
+        cfg.radius = r;
+        cfg.iterations = iterations;
+        cfg.variant = filter == 1   ? osbf::FilterVariant::OsbfFast
+                      : filter == 2 ? osbf::FilterVariant::Box
+                                    : osbf::FilterVariant::OsbfExact;
+        cfg.validate();
+        const osbf::MultiChannelImage out = osbf::filter_multichannel(img, cfg);
+        osbf::write_image(out, out_path, maxval <= 255 ? 8 : 16);
         return 0;
     } catch (...) {
         return map_exception();

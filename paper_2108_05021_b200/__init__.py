@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     SubWindowId,
     box_filter,
     box_filter_3d,
+    smooth_raster,
     build_sat,
     default_context,
     fast_osbf,
@@ -34,7 +35,7 @@ from .api import (  # noqa: F401
 
 __all__ = [
     "build", "lib", "Context", "default_context", "osbf", "osbf_step", "fast_osbf", "box_filter",
-    "osbf_3d", "box_filter_3d",
+    "osbf_3d", "box_filter_3d", "smooth_raster",
     "filter_multichannel",
     "build_sat", "subwindow_means", "sub_windows", "SubWindowId", "FilterConfig", "FilterVariant",
     "set_max_threads", "max_threads", "OsbfError", "InvalidArgument", "DomainError", "OutOfRange",

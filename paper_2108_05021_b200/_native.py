@@ -77,6 +77,9 @@ SIGNATURES = [
     ("osbf_gpu_box_filter_3d_host", _c_int,
      [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
     ("osbf_gpu_svt_host", _c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_void_p]),
+    ("osbf_gpu_smooth_raster_host", _c_int,
+     [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+      _c_void_p, _c_int]),
     ("osbf_gpu_box_filter_host", _c_int,
      [_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int]),
     ("osbf_gpu_filter_multichannel_box_host", _c_int,

@@ -425,6 +425,32 @@ class Context:
                 self.handle, ins, ous, len(chans), w, h, radius, iterations, _mode_code(mode)))
         return outs
 
+    def smooth_raster(self, raster: np.ndarray, filter: str = "osbf", radius: int = 2,
+                      iterations: int = 10, out_bits: int = 8, mode="exact") -> np.ndarray:
+        """The `osbf smooth` edge (tools/osbf_main.cpp:63-83): decoded PGM/PPM
+        samples, (H, W) or (H, W, 3) uint8/uint16, promoted, filtered with
+        "osbf" / "fast-osbf" / "box" and quantised (io.hpp:108-115) to
+        out_bits 8 or 16 — promotion and quantisation on the GPU."""
+        if filter not in _SMOOTH_FILTERS:
+            raise InvalidArgument(f"unknown filter: {filter}")
+        r = np.ascontiguousarray(raster)
+        if r.dtype not in (np.uint8, np.uint16):
+            raise InvalidArgument("raster samples must be uint8 or uint16")
+        if r.ndim == 2:
+            h, w, c = r.shape[0], r.shape[1], 1
+        elif r.ndim == 3:
+            h, w, c = r.shape
+        else:
+            raise InvalidArgument("expected an (H, W) or (H, W, C) raster")
+        if out_bits not in (8, 16):
+            raise InvalidArgument("write_image: bit depth must be 8 or 16")
+        out = np.empty(r.shape, dtype=np.uint8 if out_bits == 8 else np.uint16)
+        _check(self._lib.osbf_gpu_smooth_raster_host(
+            self.handle, ctypes.c_void_p(r.ctypes.data), r.dtype.itemsize, c, w, h,
+            _SMOOTH_FILTERS[filter], radius, iterations, _mode_code(mode),
+            ctypes.c_void_p(out.ctypes.data), out.dtype.itemsize))
+        return out
+
     def sat_host(self, plane: np.ndarray) -> np.ndarray:
         p = np.ascontiguousarray(plane, dtype=np.float64)
         h, w = p.shape
@@ -552,6 +578,16 @@ def filter_multichannel(channels, config: FilterConfig, mode="exact"):
         return ctx.iterate(stack, config.radius, config.iterations, mode)
     return default_context().filter_multichannel_host(chans, config.radius, config.iterations,
                                                       mode, variant=config.variant)
+
+
+_SMOOTH_FILTERS = {"osbf": 0, "fast-osbf": 1, "box": 2}  # osbf_filter (osbf_gpu.h)
+
+
+def smooth_raster(raster, filter: str = "osbf", radius: int = 2, iterations: int = 10,
+                  out_bits: int = 8, mode="exact"):
+    """tools/osbf_main.cpp:63-83 minus the file I/O: promote, filter_multichannel,
+    quantise — see Context.smooth_raster."""
+    return default_context().smooth_raster(raster, filter, radius, iterations, out_bits, mode)
 
 
 def build_sat(plane):

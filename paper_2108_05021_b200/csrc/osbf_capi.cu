@@ -1014,6 +1014,70 @@ osbf_status osbf_gpu_filter_multichannel_box_host(osbf_ctx* ctx, const double* c
                              OSBF_MODE_EXACT);
 }
 
+osbf_status osbf_gpu_smooth_raster_host(osbf_ctx* ctx, const void* h_raster, int sample_bytes,
+                                        int channels, int width, int height, osbf_filter filter,
+                                        int radius, int iterations, osbf_mode mode, void* h_out,
+                                        int out_sample_bytes) {
+    if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
+    // FilterConfig::validate (core.hpp:244-253), then write_image's checks
+    // (io.hpp:189-194).
+    if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "FilterConfig: radius must be >= 1");
+    if (iterations < 0)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "FilterConfig: iterations must be >= 0");
+    if (filter != OSBF_FILTER_OSBF && filter != OSBF_FILTER_FAST_OSBF && filter != OSBF_FILTER_BOX)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown filter");
+    if (channels != 1 && channels != 3)
+        return fail(OSBF_ERR_INVALID_ARGUMENT,
+                    "write_image: only 1- or 3-channel images can be saved");
+    if ((sample_bytes != 1 && sample_bytes != 2) || (out_sample_bytes != 1 && out_sample_bytes != 2))
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "write_image: bit depth must be 8 or 16");
+    osbf_status st;
+    if ((st = check_geometry(width, height, 1)) != OSBF_OK) return st;
+    if (!h_raster || !h_out) return fail(OSBF_ERR_INVALID_ARGUMENT, "null host pointer");
+    OSBF_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t plane = static_cast<size_t>(width) * height;
+    const size_t in_bytes = plane * channels * sample_bytes;
+    const size_t out_bytes = plane * channels * out_sample_bytes;
+    // host_in: the raster, then (multi-channel or 16-bit) its channel planes
+    // (uint8 for 8-bit samples — promoted inside the first pass — fp64 for
+    // 16-bit); host_out: the filtered fp64 planes, then the quantised raster.
+    const size_t planes_off = (in_bytes + 255) & ~size_t(255);
+    const bool direct = channels == 1 && sample_bytes == 1;  // already a uint8 plane
+    const size_t plane_bytes = plane * channels * (sample_bytes == 1 ? 1 : sizeof(double));
+    OSBF_CUDA(ctx->host_in.ensure(planes_off + (direct ? 0 : plane_bytes)), "alloc input");
+    const size_t raster_off = plane * channels * sizeof(double);
+    OSBF_CUDA(ctx->host_out.ensure(raster_off + out_bytes), "alloc output");
+    cudaStream_t s = ctx->stream;
+    char* in_base = static_cast<char*>(ctx->host_in.ptr);
+    double* dout = ctx->host_out.as<double>();
+    void* draster_out = static_cast<char*>(ctx->host_out.ptr) + raster_off;
+    OSBF_CUDA(cudaMemcpyAsync(in_base, h_raster, in_bytes, cudaMemcpyHostToDevice, s), "H2D");
+    const void* src = in_base;
+    const osbf_dtype dtype = sample_bytes == 1 ? OSBF_U8 : OSBF_F64;
+    if (!direct) {
+        OSBF_CUDA(osbf_gpu::raster_to_planes(in_base, sample_bytes, channels, plane,
+                                             in_base + planes_off, s, ctx->lc),
+                  "raster_to_planes");
+        src = in_base + planes_off;
+    }
+    // Channels are independent (filters2d.hpp:376-384): one batched launch.
+    st = filter == OSBF_FILTER_FAST_OSBF
+             ? osbf_gpu_fast_osbf(ctx, dtype, src, width, plane, dout, width, plane, width,
+                                  height, channels, radius, iterations, s)
+         : filter == OSBF_FILTER_BOX
+             ? osbf_gpu_box_filter(ctx, dtype, src, width, plane, dout, width, plane, width,
+                                   height, channels, radius, iterations, s)
+             : osbf_gpu_iterate(ctx, dtype, src, width, plane, dout, width, plane, width, height,
+                                channels, radius, iterations, mode, s);
+    if (st != OSBF_OK) return st;
+    OSBF_CUDA(osbf_gpu::planes_to_raster(dout, channels, plane, draster_out, out_sample_bytes, s,
+                                         ctx->lc),
+              "planes_to_raster");
+    OSBF_CUDA(cudaMemcpyAsync(h_out, draster_out, out_bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    OSBF_CUDA(cudaStreamSynchronize(s), "sync");
+    return OSBF_OK;
+}
+
 osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int height,
                               double* h_cumsum) {
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");

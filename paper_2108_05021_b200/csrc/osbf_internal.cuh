@@ -112,6 +112,15 @@ cudaError_t filter3d_pass(const double* in, int W, int H, int D, int r, bool osb
                           double* rowp, double* table, double* out, cudaStream_t s,
                           LaunchCounter& lc);
 
+// ---- smooth edge (osbf_edge.cu) --------------------------------------------
+// Interleaved uint8/uint16 raster (sample_bytes 1/2) -> channel planes
+// [channels][pixels] (uint8 planes for 8-bit samples, fp64 for 16-bit);
+// fp64 planes -> raster, quantised like io.hpp:108-115 with maxval 255 / 65535.
+cudaError_t raster_to_planes(const void* raster, int sample_bytes, int channels, size_t pixels,
+                             void* planes, cudaStream_t s, LaunchCounter& lc);
+cudaError_t planes_to_raster(const double* planes, int channels, size_t pixels, void* raster,
+                             int sample_bytes, cudaStream_t s, LaunchCounter& lc);
+
 // ---- fast mode (osbf_fast.cu) --------------------------------------------
 // Largest radius with a compiled fast-mode kernel (64x64 tile + halo in smem).
 constexpr int kFastMaxRadius = 16;

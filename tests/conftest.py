@@ -58,6 +58,10 @@ def filter3d_golden_cases():
     return sorted(glob.glob(os.path.join(GOLDEN_DIR, "filters3d", "*.npz")))
 
 
+def smooth_golden_cases():
+    return sorted(glob.glob(os.path.join(GOLDEN_DIR, "smooth", "*.npz")))
+
+
 def load_golden(path):
     d = np.load(path)
     return {k: d[k] for k in d.files}

@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <functional>
 #include <random>
 #include <stdexcept>
@@ -438,6 +440,86 @@ int main() {
         return max_abs_diff(osbf::osbf_3d(v, 2, 0), v) == 0.0 &&
                throws<std::invalid_argument>([&] { osbf::osbf_3d(v, 0, 1); }) &&
                throws<std::invalid_argument>([&] { osbf::box_filter_3d(v, 1, -1); });
+    });
+
+    // ---- smooth edge: test_cli.cpp:97-114 through smooth_file, and the
+    //      GPU raster path against the oracle restatement
+    run("smooth_file keeps a step bit-identical; zero iterations copy; errors", [] {
+        const std::string dir = std::filesystem::temp_directory_path().string();
+        const std::string in = dir + "/osbf_dropin_step.pgm", out = dir + "/osbf_dropin_out.pgm";
+        osbf::gpu::Raster step;
+        step.width = step.height = 64;
+        step.u8.resize(64 * 64);
+        for (int y = 0; y < 64; ++y)
+            for (int x = 0; x < 64; ++x) step.u8[static_cast<size_t>(y) * 64 + x] = x < 32 ? 0 : 100;
+        osbf::gpu::write_raster(step, in);
+        osbf::FilterConfig cfg;  // osbf, r=2, 10 iterations (the CLI defaults)
+        osbf::gpu::smooth_file(in, out, cfg);
+        if (osbf::gpu::read_raster(out).u8 != step.u8) return false;
+        cfg.variant = osbf::FilterVariant::Box;
+        cfg.iterations = 0;
+        osbf::gpu::smooth_file(in, out, cfg);
+        const auto back = osbf::gpu::read_raster(out);
+        std::filesystem::remove(in);
+        std::filesystem::remove(out);
+        cfg.variant = osbf::FilterVariant::Gaussian;
+        return back.u8 == step.u8 && back.maxval == 255 &&
+               throws<std::invalid_argument>([&] { osbf::gpu::smooth(step, cfg); }) &&
+               throws<osbf::gpu::ParseError>([&] { osbf::gpu::read_raster(in + ".missing.pgm"); }) ==
+                   false;
+    });
+    run("smooth (GPU promote/filter/quantise) byte-identical to the oracle; u8 RGB and u16", [] {
+        std::mt19937_64 rng(81);
+        for (int wide = 0; wide < 2; ++wide)
+            for (int f = 0; f < 3; ++f) {
+                osbf::gpu::Raster r;
+                r.width = 45;
+                r.height = 31;
+                r.channels = wide ? 1 : 3;
+                r.maxval = wide ? 65535 : 255;
+                const size_t n = r.sample_count();
+                if (wide) {
+                    r.u16.resize(n);
+                    for (auto& v : r.u16) v = static_cast<uint16_t>(rng() >> 48);
+                } else {
+                    r.u8.resize(n);
+                    for (auto& v : r.u8) v = static_cast<uint8_t>(rng() >> 56);
+                }
+                osbf::FilterConfig cfg;
+                cfg.radius = 2 + f;
+                cfg.iterations = 3;
+                cfg.variant = f == 0 ? osbf::FilterVariant::OsbfExact
+                              : f == 1 ? osbf::FilterVariant::OsbfFast
+                                       : osbf::FilterVariant::Box;
+                const auto got = osbf::gpu::smooth(r, cfg);
+                std::vector<uint16_t> want16(n);
+                std::vector<uint8_t> want8(n);
+                const void* src = wide ? static_cast<const void*>(r.u16.data()) : r.u8.data();
+                void* dst = wide ? static_cast<void*>(want16.data()) : want8.data();
+                if (oracle_smooth_raster(src, wide ? 2 : 1, r.channels, r.width, r.height, f,
+                                         cfg.radius, cfg.iterations, dst, wide ? 2 : 1) != 0)
+                    return false;
+                if (wide ? got.u16 != want16 : got.u8 != want8) return false;
+            }
+        return true;
+    });
+    run("read_raster: netpbm header rules and errors as read_image", [] {
+        const std::string p = std::filesystem::temp_directory_path().string() + "/osbf_dropin.pnm";
+        auto put = [&](const std::string& bytes) {
+            std::ofstream(p, std::ios::binary) << bytes;
+        };
+        put("P2\n# comment\n3 1 # more\n9\n0 4 9\n");
+        const auto a = osbf::gpu::read_raster(p);
+        if (a.width != 3 || a.u8 != std::vector<uint8_t>{0, 4, 9}) return false;
+        put(std::string("P5\n2 1\n65535\n") + std::string("\x01\x02\xff\xfe", 4));
+        const auto b = osbf::gpu::read_raster(p);
+        if (b.u16 != std::vector<uint16_t>{0x0102, 0xfffe}) return false;
+        bool ok = true;
+        for (const char* bad : {"P7\n1 1\n255\n", "P5\n0 1\n255\n", "P5\n1 1\n70000\n",
+                                "P5\n2 2\n255\nab", "P2\n1 1\n5\n6\n", "P2\n1 1\n"})
+            ok = ok && (put(bad), throws<osbf::gpu::ParseError>([&] { osbf::gpu::read_raster(p); }));
+        std::filesystem::remove(p);
+        return ok;
     });
 
     std::printf("%d failure(s)\n", failures);

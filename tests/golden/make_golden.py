@@ -133,6 +133,24 @@ def filter3d_cases():
     return out
 
 
+def smooth_cases():
+    """(name, raster, filter, r, iterations) for the `osbf smooth` edge
+    (tools/osbf_main.cpp:63-83), run through the reference's own file I/O."""
+    rng = np.random.default_rng(37)
+    step = np.where(np.arange(64)[None, :] < 32, 0, 100).astype(np.uint8) * np.ones((64, 1), np.uint8)
+    board = ((np.arange(48)[:, None] // 6 + np.arange(40)[None, :] // 6) % 2 * 255).astype(np.uint8)
+    return [
+        ("step_64_osbf_r2_it10", step, "osbf", 2, 10),  # test_cli.cpp:97-106
+        ("board_box_it0", board, "box", 2, 0),  # test_cli.cpp:108-114
+        ("rgb_u8_osbf_r2", (rng.random((37, 29, 3)) * 256).astype(np.uint8), "osbf", 2, 3),
+        ("rgb_u8_fast_r3", (rng.random((23, 41, 3)) * 256).astype(np.uint8), "fast-osbf", 3, 2),
+        ("rgb_u8_box_r1", (rng.random((19, 17, 3)) * 256).astype(np.uint8), "box", 1, 4),
+        ("gray_u16_osbf_r4", (rng.random((33, 35)) * 65536).astype(np.uint16), "osbf", 4, 2),
+        ("gray_u16_box_r2", (rng.random((9, 70)) * 65536).astype(np.uint16), "box", 2, 1),
+        ("row_u8_osbf_r3", (rng.random((1, 50)) * 256).astype(np.uint8), "osbf", 3, 2),
+    ]
+
+
 def main() -> None:
     ref = Reference()
     ref.set_max_threads(1)
@@ -170,6 +188,15 @@ def main() -> None:
                             output=out, radius=r, iterations=iters, osbf3=osbf3,
                             svt=ref.svt(vol))
         print(f"filters3d/{name:28s} {vol.shape} r={r} it={iters}")
+    os.makedirs(os.path.join(HERE, "smooth"), exist_ok=True)
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, raster, filt, r, iters in smooth_cases():
+            out = ref.smooth_raster(raster, filt, r, iters, tmp)
+            np.savez_compressed(os.path.join(HERE, "smooth", f"{name}.npz"), input=raster,
+                                output=out, filter=filt, radius=r, iterations=iters)
+            print(f"smooth/{name:24s} {raster.shape} {raster.dtype} {filt} r={r} it={iters}")
     # integral.hpp / test_integral.cpp:19-29 known SAT
     p = np.array([[1.0, 2.0], [3.0, 4.0]])
     np.savez_compressed(os.path.join(HERE, "sat_2x2.npz"), input=p, cumsum=ref.sat(p))
