@@ -445,11 +445,16 @@ __global__ void __launch_bounds__(NT, 2)
         }
         const int xa = xs + seg * SW;
         double acc = c[seg * BR + rr];  // R(xa - 1)
+        // operands first: the chain then waits on DADD latency only (the
+        // shared loads cannot be hoisted past the rb stores by the compiler)
+        double uv[SW];
+#pragma unroll
+        for (int i = 0; i < SW; ++i) uv[i] = xa + i <= xe ? u[seg * SW + i] : 0.0;
 #pragma unroll
         for (int i = 0; i < SW; ++i) {
             const int x = xa + i;
             if (x <= xe) {
-                acc = __dadd_rn(acc, u[seg * SW + i]);  // row += src[x]
+                acc = __dadd_rn(acc, uv[i]);  // row += src[x]
                 const int j = x - jbase;
                 if (j >= 0 && j < L::NCC) rb[j] = acc;
             }
@@ -493,8 +498,21 @@ __global__ void __launch_bounds__(NT, 2)
             if (tid < L::NCC) {
                 const int cx = X0 - R + tid;
                 if (cx >= 0 && cx <= W) {
-                    for (int rr = 0; rr < nrows; ++rr) {
-                        creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);  // above[x+1] + row
+                    int rr = 0;
+                    // full 8-row chunks with the row sums loaded ahead (see row_prefix)
+                    for (; rr + 8 <= nrows; rr += 8) {
+                        double rv[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) rv[i] = Rb[(rr + i) * L::PR + tid];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            creg = __dadd_rn(creg, rv[i]);  // above[x+1] + row
+                            unsafe_here |= !table_value_safe(creg);
+                            Cr[ring_row<L>(y0 + rr + i + 1) * L::NCC + tid] = creg;
+                        }
+                    }
+                    for (; rr < nrows; ++rr) {
+                        creg = __dadd_rn(creg, Rb[rr * L::PR + tid]);
                         unsafe_here |= !table_value_safe(creg);
                         Cr[ring_row<L>(y0 + rr + 1) * L::NCC + tid] = creg;
                     }
