@@ -10,8 +10,9 @@
 // reference's inclusion-exclusion order, IEEE division by the clipped count,
 // |a - u| and the strict-< first minimum in filters3d.hpp:29-51 order.
 //
-// Per pass (256^3): svt_rows ~55 us (HBM-streaming), svt_yz ~215 us (one
-// barrier per wavefront step), filter3d ~800 us — fp64-latency/L1 bound:
+// Per pass (256^3): svt_rows ~55 us (HBM-streaming), svt_yz ~180 us (one
+// barrier per wavefront step; 2 columns x 128 plane slots per CTA measured
+// best: 4 columns 214 us, 1 column 288 us), filter3d ~800 us — fp64-latency/L1 bound:
 // 64 distinct table corners, 98 dependent-chain DADDs and 14 divisions per
 // voxel, not an HBM roofline kernel.
 #include "osbf_exact2_kernel.cuh"  // div_by_count
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kRowsCta)
 // earlier), prefetched PF steps ahead with cp.async together with the row
 // prefixes.
 // T(y-1, z) and T(y-1, z-1) stay in registers.
-constexpr int kSvtXL = 4, kSvtPL = 8, kSvtNW = 16, kSvtPF = 8;
+constexpr int kSvtXL = 2, kSvtPL = 16, kSvtNW = 8, kSvtPF = 8;
 constexpr int kSvtNP = kSvtPL * kSvtNW;
 
 struct SvtCursor {  // plane slot position: row y (negative while waiting), plane z
