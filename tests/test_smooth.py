@@ -99,3 +99,14 @@ def test_smooth_gpu_fast_mode_and_errors(ctx, oracle_lib):
         ctx.smooth_raster(np.zeros((4, 4, 2), np.uint8))  # 2 channels cannot be saved
     with pytest.raises(ob.InvalidArgument):
         ctx.smooth_raster(np.zeros((4, 4), np.float32))
+
+
+@pytest.mark.gpu
+def test_smooth_gpu_c2_size_rgb(ctx, oracle_lib):
+    """C2's shape (1920 x 1080 x 3) through the edge, byte-identical to the
+    oracle; r=3 like C2, 3 iterations so the CPU checker stays a few seconds."""
+    x = (np.random.default_rng(74).random((1080, 1920, 3)) * 256).astype(np.uint8)
+    assert np.array_equal(ctx.smooth_raster(x, "osbf", 3, 3), oracle_lib.smooth_raster(x, "osbf", 3, 3))
+    y = (np.random.default_rng(75).random((1080, 1920)) * 65536).astype(np.uint16)
+    assert np.array_equal(ctx.smooth_raster(y, "box", 3, 2, out_bits=16),
+                          oracle_lib.smooth_raster(y, "box", 3, 2, 16))
