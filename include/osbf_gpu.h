@@ -71,6 +71,18 @@ typedef struct osbf_ctx osbf_ctx;
 int osbf_gpu_abi_version(void);
 /* Thread-local text of the last failure on this thread ("" if none). */
 const char* osbf_gpu_last_error(void);
+
+/* Name of the kernel family that ran the last pass issued by this host thread
+ * (e.g. "fast_strip", "fast_tma_step", "exact_strip"); instrumentation for
+ * tests and the benchmark, no reference counterpart. */
+const char* osbf_gpu_last_kernel(void);
+
+/* Diagnostics: force the kernel family of fast passes process-wide ("strip",
+ * "tile", "tma", "stream", "sep"; NULL or "" = per-radius default).  A family
+ * that does not apply to a pass (radius, layout) falls through to the
+ * default order.  No reference counterpart; results stay within fast mode's
+ * tolerance whichever family runs. */
+osbf_status osbf_gpu_set_fast_kernel(const char* name);
 /* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
 int osbf_gpu_device_available(void);
 

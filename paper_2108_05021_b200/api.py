@@ -181,6 +181,19 @@ class Context:
     def launches(self) -> int:
         return int(self._lib.osbf_gpu_ctx_launch_count(self.handle))
 
+    @staticmethod
+    def set_fast_kernel(name: str | None) -> None:
+        """Diagnostics: force the fast-pass kernel family process-wide
+        (osbf_gpu_set_fast_kernel): "strip", "tile", "tma", "stream", "sep",
+        or None for the per-radius default."""
+        _check(N.lib().osbf_gpu_set_fast_kernel((name or "").encode()))
+
+    @property
+    def last_kernel(self) -> str:
+        """Kernel family of the last pass issued from this thread
+        (osbf_gpu_last_kernel), e.g. ``fast_strip``."""
+        return self._lib.osbf_gpu_last_kernel().decode()
+
     def set_temporal_blocking(self, passes_per_launch: int) -> None:
         """Fast mode: 2 = two passes per launch (radius <= 2), 1 = default."""
         _check(self._lib.osbf_gpu_ctx_set_temporal_blocking(self.handle, passes_per_launch))

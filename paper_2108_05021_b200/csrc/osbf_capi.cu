@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 namespace {
 
 thread_local std::string g_last_error;
+thread_local const char* g_last_kernel = "";
 
 osbf_status fail(osbf_status st, const char* fmt, ...) {
     char buf[512];
@@ -200,6 +202,13 @@ __global__ void convert_kernel(const T* __restrict__ in, size_t ip, size_t ipl,
 }  // namespace
 
 namespace osbf_gpu {
+void note_kernel(const char* name) { g_last_kernel = name; }
+
+namespace {
+std::atomic<const char*> g_fast_override{nullptr};
+}
+const char* fast_kernel_override() { return g_fast_override.load(std::memory_order_acquire); }
+
 cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t op,
                            size_t opl, cudaStream_t s, LaunchCounter& lc) {
     dim3 grid((g.width + 255) / 256, g.height, g.batch);
@@ -350,6 +359,22 @@ extern "C" {
 int osbf_gpu_abi_version(void) { return OSBF_GPU_ABI_VERSION; }
 
 const char* osbf_gpu_last_error(void) { return g_last_error.c_str(); }
+
+const char* osbf_gpu_last_kernel(void) { return g_last_kernel; }
+
+osbf_status osbf_gpu_set_fast_kernel(const char* name) {
+    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "stream", "sep"};
+    if (!name || !name[0]) {
+        osbf_gpu::g_fast_override.store(nullptr, std::memory_order_release);
+        return OSBF_OK;
+    }
+    for (const char* k : kNames)
+        if (std::strcmp(k, name) == 0) {
+            osbf_gpu::g_fast_override.store(k, std::memory_order_release);
+            return OSBF_OK;
+        }
+    return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown fast kernel family '%s'", name);
+}
 
 int osbf_gpu_device_available(void) { return device_ok() ? 1 : 0; }
 

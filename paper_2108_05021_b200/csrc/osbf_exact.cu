@@ -177,6 +177,7 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
                          double* out, size_t out_pitch, size_t out_plane, double* means,
                          uint8_t* sel, cudaStream_t s, LaunchCounter& lc) {
     ++lc.launches;
+    note_kernel("exact_row_prefix+exact_col_chain+exact_select");
     switch (in.dtype) {
         case OSBF_U8:
             return launch_stencil<uint8_t>(in, g, radius, sat, out, out_pitch, out_plane, means,
@@ -261,6 +262,7 @@ cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius,
                              double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
                              LaunchCounter& lc) {
     if (radius < 1 || radius > kExactFusedMaxRadius) return cudaErrorInvalidValue;
+    note_kernel("exact_row_carries+exact_strip");
     const int nsc = g.width / ex2::SW + 1;
     cudaError_t e;
     switch (in.dtype) {

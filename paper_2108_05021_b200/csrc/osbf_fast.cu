@@ -42,6 +42,24 @@ bool encode_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, ui
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+bool encode_rows_4d(CUtensorMap* map, CUtensorMapDataType dtype, size_t elem_bytes,
+                    const void* base, uint64_t width, uint64_t height, uint64_t planes,
+                    uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t vec, uint32_t box_groups,
+                    uint32_t box_h) {
+    auto fn = encode_fn();
+    if (!fn || vec == 0 || width % vec != 0) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0) return false;
+    if ((vec * elem_bytes) % 16 != 0) return false;
+    if (pitch_bytes % 16 != 0 || plane_bytes % 16 != 0) return false;
+    if (box_groups > 256 || box_h > 256 || vec > 256) return false;
+    const cuuint64_t dims[4] = {vec, width / vec, height, planes};
+    const cuuint64_t strides[3] = {vec * elem_bytes, pitch_bytes, plane_bytes};
+    const cuuint32_t box[4] = {vec, box_groups, box_h, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, dtype, 4, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace tma
 
 template <int R>

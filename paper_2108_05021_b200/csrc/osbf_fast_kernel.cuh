@@ -42,6 +42,8 @@
 // reference's a_m; the tolerance is checked in tests).  uint8 input
 // (EXACT_DIV): sums are exact integers in any order, a_i = S_i/n_i is IEEE,
 // d_i = |a_i - u| and the output is a_m -> bit-identical to the reference.
+#include <string.h>
+
 #include "osbf_internal.cuh"
 #include "osbf_tma.cuh"
 
@@ -211,7 +213,7 @@ struct ColFactors {
 
 // Means, |a-u| selection and the store for one pixel (S = the eight window
 // sums in reference order, u = the centre sample).
-template <int R, bool EXACT_DIV, bool BORDER, bool DIAG>
+template <int R, bool EXACT_DIV, bool BORDER, bool DIAG, bool FAST_SEQ = false>
 __device__ __forceinline__ double select_store(const double (&S)[8], double u, int gx, int gy,
                                              int W, int H, int b, double* __restrict__ o,
                                              double* __restrict__ means,
@@ -266,15 +268,30 @@ __device__ __forceinline__ double select_store(const double (&S)[8], double u, i
 #pragma unroll
         for (int i = 0; i < 8; ++i) rc[i] = i < 4 ? kRq : kRh;
     }
-    // d_i = S_i/n_i - u in one rounding; a stable tournament keeps the first
-    // minimum of |d_i| (filters2d.hpp:78 strict <) at depth 3.  Finite input
-    // assumed (non-finite samples: use exact mode).
-    double d[8];
+    // d_i = S_i/n_i - u in one rounding; the first minimum of |d_i|
+    // (filters2d.hpp:78 strict <), output u + d_m.  (Carrying S_m to output
+    // S_m / n_m costs 14 selects per pixel, measured 11-14% of a pass on
+    // these issue-bound kernels; the result is within 1 ulp of it and the
+    // sums themselves already differ from the reference's whole-image table
+    // by rounding.)  FAST_SEQ: a sequential strict-< scan (2 live values, for
+    // register-capped kernels); else a stable depth-3 tournament.  Finite
+    // input assumed (non-finite samples: use exact mode).
+    double best;
+    if constexpr (FAST_SEQ) {
+        best = fma(S[0], rc[0], -u);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = fma(S[i], rc[i], -u);
-    auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
-    const double best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
-                             pick(pick(d[4], d[5]), pick(d[6], d[7])));
+        for (int i = 1; i < 8; ++i) {
+            const double d = fma(S[i], rc[i], -u);
+            best = fabs(d) < fabs(best) ? d : best;
+        }
+    } else {
+        double d[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] = fma(S[i], rc[i], -u);
+        auto pick = [](double a, double c) { return fabs(c) < fabs(a) ? c : a; };
+        best = pick(pick(pick(d[0], d[1]), pick(d[2], d[3])),
+                    pick(pick(d[4], d[5]), pick(d[6], d[7])));
+    }
     const double v = u + best;
     *o = v;
     return v;
@@ -429,6 +446,7 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
     if (cudaError_t e = ensure_smem(fast_sep_step<R, T, EXACT_DIV, DIAG>, smem, done))
         return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    note_kernel(DIAG ? "fast_sep_step (diagnostics)" : "fast_sep_step");
     fast_sep_step<R, T, EXACT_DIV, DIAG><<<grid, NT, smem, s>>>(
         static_cast<const T*>(in.base), in.pitch, in.plane, out, op, opl, means, sel, g.width,
         band_of(g));
@@ -450,11 +468,11 @@ cudaError_t launch_r(const PlaneView& in, const Geometry& g, double* out, size_t
 constexpr int kTmaRadius = 4;
 constexpr int kTb2Radius = 2;
 
-template <int R, typename T>
+template <int R, typename T, int THT_ = 0>
 struct TLay {
     // taller tiles for larger radii: (SEGT + 2R) / SEGT rows are touched per
     // output row of a column segment
-    static constexpr int THT = R <= 2 ? 64 : 128;
+    static constexpr int THT = THT_ ? THT_ : (R <= 2 ? 64 : 128);
     static constexpr int SEGT = THT / NSB;
     static constexpr int LH = THT + 2 * R;
     static constexpr int LWU = TW + 2 * R;
@@ -471,11 +489,10 @@ struct TLay {
     static constexpr size_t SMEM = TILE_BYTES + 128;  // + alignment slack
 };
 
-template <int R, typename T, bool EXACT_DIV, bool BORDER>
+template <int R, typename T, bool EXACT_DIV, bool BORDER, class Ly = TLay<R, T>, bool SEQ = false>
 __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, int Y0, int W,
                                             const Band& band, int b, double* __restrict__ outp,
                                             size_t out_pitch, const double* __restrict__ rtab) {
-    using Ly = TLay<R, T>;
     const int x = threadIdx.x % TW, s = threadIdx.x / TW;
     const int gx = X0 + x;
     if (BORDER && gx >= W) return;
@@ -516,18 +533,29 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
                                  P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
                                  P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
                                  Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
-            select_store<R, EXACT_DIV, BORDER, false>(S, Uc[y + R], gx, gy, W, H, b, o, nullptr,
-                                                      nullptr, cf, rtab);
+            select_store<R, EXACT_DIV, BORDER, false, SEQ>(S, Uc[y + R], gx, gy, W, H, b, o,
+                                                           nullptr, nullptr, cf, rtab);
             o += out_pitch;
         }
     }
 }
 
-template <int R, typename T, bool EXACT_DIV>
-__global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3 : (R <= 4 ? 2 : 1)))
+// Tile-kernel variants: VAR 0 = depth-3 tournament, 64-row tiles (128 above
+// r = 2), register bound for 3 / 2 CTAs per SM; VAR 1 = sequential scan and
+// 64-row tiles, register bound for 4 CTAs per SM (r <= 2) / 3 (r 3..4).
+template <int R, typename T, int VAR>
+struct TVar {
+    static constexpr bool SEQ = VAR == 1;
+    using Ly = TLay<R, T, VAR == 1 ? 64 : 0>;
+    static constexpr int MINB = VAR == 1 ? (R <= 2 ? 4 : 3) : (R <= 2 ? 3 : (R <= 4 ? 2 : 1));
+};
+
+template <int R, typename T, bool EXACT_DIV, int VAR = 0>
+__global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : TVar<R, T, VAR>::MINB)
     fast_tma_step(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
                   size_t out_pitch, size_t out_plane, int W, Band band) {
-    using Ly = TLay<R, T>;
+    using Ly = typename TVar<R, T, VAR>::Ly;
+    constexpr bool SEQ = TVar<R, T, VAR>::SEQ;
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ double rtab[Ly::NRT];
@@ -545,9 +573,9 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : (R <= 2 ? 3
     double* outp = out + static_cast<size_t>(b) * out_plane;
     if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
         Y0 + Ly::THT <= band.y_end)
-        direct_walk<R, T, EXACT_DIV, false>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
+        direct_walk<R, T, EXACT_DIV, false, Ly, SEQ>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
     else
-        direct_walk<R, T, EXACT_DIV, true>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
+        direct_walk<R, T, EXACT_DIV, true, Ly, SEQ>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
     if (band.push_rows) {  // row-band mode with the fused halo push
         const int gx = X0 + threadIdx.x % TW, ya = Y0 + (threadIdx.x / TW) * Ly::SEGT;
         if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
@@ -562,20 +590,178 @@ constexpr CUtensorMapDataType tma_dtype() {
 }
 
 // Returns cudaErrorNotSupported (no launch) when the layout is not TMA-able.
-template <int R, typename T, bool EXACT_DIV>
+template <int R, typename T, bool EXACT_DIV, int VAR = 0>
 cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size_t op,
                        size_t opl, cudaStream_t s) {
-    using Ly = TLay<R, T>;
+    using Ly = typename TVar<R, T, VAR>::Ly;
     CUtensorMap map;
     const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
     if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
                         in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
         return cudaErrorNotSupported;
     static std::atomic<unsigned long long> done{0};
-    if (cudaError_t e = ensure_smem(fast_tma_step<R, T, EXACT_DIV>, Ly::SMEM, done)) return e;
+    if (cudaError_t e = ensure_smem(fast_tma_step<R, T, EXACT_DIV, VAR>, Ly::SMEM, done)) return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
-    fast_tma_step<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
-                                                              band_of(g));
+    note_kernel(VAR ? "fast_tma_step (seq)" : "fast_tma_step");
+    fast_tma_step<R, T, EXACT_DIV, VAR><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                                   band_of(g));
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Persistent tile kernel (r <= kTmaRadius): the same per-tile computation as
+// fast_tma_step (bit-identical outputs), but a grid of #SMs x occupancy CTAs
+// walks the tiles round robin with two shared-memory tile buffers, so the TMA
+// load of a CTA's next tile is in flight while it computes the current one
+// (fast_tma_step waited for every tile's load: ~25% of its stall samples).
+template <int R, typename T>
+struct PLay {
+    using Base = TLay<R, T>;
+    static constexpr int THT = 64;
+    static constexpr int SEGT = THT / NSB;
+    static constexpr int LH = THT + 2 * R;
+    static constexpr int RA = Base::RA, XOFF = Base::XOFF, BW = Base::BW;
+    static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
+    static constexpr size_t BUF = (TILE_BYTES + 127) / 128 * 128;
+    static constexpr int NRT = 2 * R + 2;
+    static constexpr size_t SMEM = 128 + 2 * BUF;
+    static constexpr int MINB = R <= 2 ? 3 : 2;
+};
+
+template <int R, typename T, bool EXACT_DIV, bool BORDER>
+__device__ __forceinline__ void tile_walk(const T* __restrict__ Us, int X0, int Y0, int W,
+                                          const Band& band, double* __restrict__ outp,
+                                          size_t out_pitch, const double* __restrict__ rtab) {
+    using Ly = PLay<R, T>;
+    const int x = threadIdx.x % TW, s = threadIdx.x / TW;
+    const int gx = X0 + x;
+    if (BORDER && gx >= W) return;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (BORDER) {
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    const int y0 = s * Ly::SEGT;
+    const T* __restrict__ col = Us + y0 * Ly::BW + x + Ly::XOFF;
+    const int H = band.h_img;
+    double* o = outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
+    constexpr int NJ = Ly::SEGT + 2 * R;
+    double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
+    P1[0] = P2[0] = Q[0] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        double v[2 * R + 1];
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) v[i] = to_f64(col[j * Ly::BW + i]);
+        double a = v[0], c = v[R];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) {
+            a += v[i];
+            c += v[R + i];
+        }
+        const double e = v[R];
+        Uc[j] = e;
+        P1[j + 1] = P1[j] + a;
+        P2[j + 1] = P2[j] + c;
+        Q[j + 1] = Q[j] + ((a + c) - e);
+        const int y = j - 2 * R;
+        if (y >= 0) {
+            const int gy = Y0 + y0 + y;
+            if (BORDER && gy >= band.y_end) break;
+            const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                 P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                 P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                 Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+            select_store<R, EXACT_DIV, BORDER, false>(S, Uc[y + R], gx, gy, W, H, 0, o, nullptr,
+                                                      nullptr, cf, rtab);
+            o += out_pitch;
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+__global__ void __launch_bounds__(NT, PLay<R, T>::MINB)
+    fast_tile(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+              size_t out_pitch, size_t out_plane, int W, Band band, int ntx, int nty,
+              int ntiles) {
+    using Ly = PLay<R, T>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar[2];
+    __shared__ double rtab[Ly::NRT];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    unsigned char* sm = smem_raw + ((128u - (base & 127u)) & 127u);
+    T* bufs[2] = {reinterpret_cast<T*>(sm), reinterpret_cast<T*>(sm + Ly::BUF)};
+    const int tid = threadIdx.x;
+    auto tile_of = [&](int t, int& X0, int& Y0, int& b) {
+        const int tx = t % ntx, rest = t / ntx;
+        X0 = tx * TW;
+        Y0 = band.y_out0 + (rest % nty) * Ly::THT;
+        b = rest / nty;
+    };
+    auto issue = [&](int t, int sl) {
+        int X0, Y0, b;
+        tile_of(t, X0, Y0, b);
+        tma::mbar_arrive_expect_tx(&bar[sl], Ly::TILE_BYTES);
+        tma::load_3d(bufs[sl], &tmap, X0 - Ly::RA, Y0 - R - band.y_in0, b, &bar[sl]);
+    };
+    if (tid == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+    }
+    if (tid < Ly::NRT) rtab[tid] = tid ? 1.0 / tid : 0.0;
+    __syncthreads();
+    if (tid == 0 && static_cast<int>(blockIdx.x) < ntiles) issue(blockIdx.x, 0);
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int sl = i & 1;
+        tma::mbar_wait(&bar[sl], (i >> 1) & 1);
+        // every thread is done with the previous tile: its buffer takes the next
+        __syncthreads();
+        if (tid == 0 && t + static_cast<int>(gridDim.x) < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(t + gridDim.x, sl ^ 1);
+        }
+        int X0, Y0, b;
+        tile_of(t, X0, Y0, b);
+        double* outp = out + static_cast<size_t>(b) * out_plane;
+        if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
+            Y0 + Ly::THT <= band.y_end)
+            tile_walk<R, T, EXACT_DIV, false>(bufs[sl], X0, Y0, W, band, outp, out_pitch, rtab);
+        else
+            tile_walk<R, T, EXACT_DIV, true>(bufs[sl], X0, Y0, W, band, outp, out_pitch, rtab);
+        if (band.push_rows) {  // row-band mode with the fused halo push
+            const int gx = X0 + tid % TW, ya = Y0 + (tid / TW) * Ly::SEGT;
+            if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+cudaError_t launch_tile(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                        size_t opl, cudaStream_t s) {
+    using Ly = PLay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+        return cudaErrorNotSupported;
+    auto* fn = fast_tile<R, T, EXACT_DIV>;
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fn, Ly::SMEM, done)) return e;
+    int dev = 0, nsm = 0, per_sm = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    if (cudaError_t e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) return e;
+    if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, Ly::SMEM))
+        return e;
+    if (per_sm < 1) return cudaErrorNotSupported;
+    const int ntx = (g.width + TW - 1) / TW, nty = (g.height + Ly::THT - 1) / Ly::THT;
+    const long long ntiles = static_cast<long long>(ntx) * nty * g.batch;
+    if (ntiles > (1ll << 31) - 1) return cudaErrorNotSupported;
+    const long long cap = static_cast<long long>(nsm) * per_sm;
+    const int grid = static_cast<int>(ntiles < cap ? ntiles : cap);
+    note_kernel("fast_tile");
+    fn<<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width, band_of(g), ntx, nty,
+                                  static_cast<int>(ntiles));
     return cudaGetLastError();
 }
 
@@ -583,15 +769,63 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
 }  // namespace osbf_gpu
 
 #include "osbf_fast_stream.cuh"
+#include "osbf_strip.cuh"
 
 namespace osbf_gpu {
 namespace fastk {
 
+// Kernel family for the fast pass.  OSBF_GPU_FAST (read once per process)
+// forces one for A/B measurements: "strip", "tile" (persistent TMA tiles),
+// "tma" (one tile per CTA), "stream" or "sep"; unset = the per-radius
+// default below.
+inline const char* fast_forced() {
+    const char* o = fast_kernel_override();
+    if (o) return o;
+    static const char* v = [] {
+        const char* e = getenv("OSBF_GPU_FAST");
+        return (e && e[0]) ? e : "";
+    }();
+    return v;
+}
+inline bool fast_allowed(const char* name, bool dflt) {
+    const char* f = fast_forced();
+    if (!f[0]) return dflt;
+    return strcmp(f, name) == 0;
+}
+
 template <int R, bool DIAG>
 cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, size_t op,
                          size_t opl, double* means, uint8_t* sel, cudaStream_t s) {
+    if constexpr (!DIAG) {
+        if (fast_allowed("strip", false)) {
+            const cudaError_t e = strip_launch_radius<R>(in, g, out, op, opl, s);
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R <= kTmaRadius && !DIAG) {
+        if (fast_allowed("tmaseq", false)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_tma<R, float, false, 1>(in, g, out, op, opl, s); break;
+                default: e = launch_tma<R, double, false, 1>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R <= kTmaRadius && !DIAG) {
+        if (fast_allowed("tile", false)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_tile<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_tile<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_tile<R, double, false>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
     if constexpr (R >= kStreamMinRadius && R <= kStreamMaxRadius && !DIAG) {
-        if (stream_enabled()) {
+        if (stream_enabled() && fast_allowed("stream", true)) {
             cudaError_t e = cudaErrorNotSupported;
             switch (in.dtype) {
                 case OSBF_U8: e = launch_stream<R, uint8_t, true>(in, g, out, op, opl, s); break;
@@ -602,13 +836,15 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
         }
     }
     if constexpr (R <= kTmaRadius && !DIAG) {
-        cudaError_t e = cudaErrorNotSupported;
-        switch (in.dtype) {
-            case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
-            case OSBF_F32: e = launch_tma<R, float, false>(in, g, out, op, opl, s); break;
-            default: e = launch_tma<R, double, false>(in, g, out, op, opl, s); break;
+        if (fast_allowed("tma", true)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_tma<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_tma<R, double, false>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
         }
-        if (e != cudaErrorNotSupported) return e;
     }
     switch (in.dtype) {
         case OSBF_U8:
@@ -806,6 +1042,7 @@ cudaError_t launch_tma2(const PlaneView& in, const Geometry& g, double* out, siz
     static std::atomic<unsigned long long> done{0};
     if (cudaError_t e = ensure_smem(fast_tma_step2<R, T, EXACT1>, Ly::SMEM, done)) return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
+    note_kernel("fast_tma_step2");
     fast_tma_step2<R, T, EXACT1><<<grid, Ly::NTT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                  band_of(g));
     return cudaGetLastError();

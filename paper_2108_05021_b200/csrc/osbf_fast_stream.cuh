@@ -279,6 +279,7 @@ cudaError_t launch_stream(const PlaneView& in, const Geometry& g, double* out, s
     const int band_rows = (R >= 10 && g.height <= 1024) ? g.height
                                                         : (g.height < 512 ? g.height : 512);
     dim3 grid(strips, (g.height + band_rows - 1) / band_rows, g.batch);
+    note_kernel("fast_stream_step");
     fast_stream_step<R, T, EXACT_DIV><<<grid, Ly::NTS, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                       band_of(g), band_rows);
     return cudaGetLastError();

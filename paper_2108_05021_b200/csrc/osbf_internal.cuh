@@ -61,6 +61,15 @@ inline cudaError_t ensure_smem(F* fn, size_t bytes, std::atomic<unsigned long lo
     return e;
 }
 
+// Name of the kernel family the last pass of this host thread launched
+// (instrumentation: osbf_gpu_last_kernel, bench labels).  Set by each
+// launcher just before its launch; a static string.
+void note_kernel(const char* name);
+
+// Process-wide override of the fast-pass kernel family (osbf_gpu_set_fast_kernel,
+// diagnostics / A-B tests); null = none.
+const char* fast_kernel_override();
+
 // Launch statistics (kernels issued) for instrumentation.
 struct LaunchCounter {
     uint64_t launches = 0;
