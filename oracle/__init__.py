@@ -209,11 +209,52 @@ class Reference:
         lib.ref_set_max_threads.argtypes = [ctypes.c_int]
         lib.ref_set_max_threads.restype = None
         lib.ref_pin_allocator_for_timing.restype = None
+        _ull = ctypes.c_ulonglong
+        lib.ref_checkerboard.argtypes = [ctypes.c_int] * 3 + [ctypes.c_double] * 3 + [_ull, _dp, _dp]
+        lib.ref_step_volume.argtypes = [ctypes.c_int] * 4 + [ctypes.c_double] * 3 + [_ull, _dp, _dp]
+        lib.ref_phantom.argtypes = [ctypes.c_int, ctypes.c_int, _dp]
+        lib.ref_psnr.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_double]
+        lib.ref_psnr.restype = ctypes.c_double
+        lib.ref_rmse.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int]
+        lib.ref_rmse.restype = ctypes.c_double
         self.lib = lib
 
     @staticmethod
     def available(path: str = REF_SO) -> bool:
         return os.path.exists(path)
+
+    # -- acceptance-criterion inputs and metrics (the reference's own code)
+    def checkerboard(self, w, h, cell, lo, hi, sigma, seed):
+        """(clean, noisy): synth.hpp:52 checkerboard + :94 Gaussian noise."""
+        c, n = np.empty((h, w)), np.empty((h, w))
+        st = self.lib.ref_checkerboard(w, h, cell, lo, hi, sigma, seed, _ptr(c), _ptr(n))
+        if st:
+            raise CheckerError(st, "ref checkerboard")
+        return c, n
+
+    def step_volume(self, w, h, d, edge, lo, hi, sigma, seed):
+        """(clean, noisy) volumes (D, H, W): synth.hpp:81 + :106."""
+        c, n = np.empty((d, h, w)), np.empty((d, h, w))
+        st = self.lib.ref_step_volume(w, h, d, edge, lo, hi, sigma, seed, _ptr(c), _ptr(n))
+        if st:
+            raise CheckerError(st, "ref step_volume")
+        return c, n
+
+    def phantom(self, w=256, h=256):
+        """tests/support/fixtures.hpp:36, the reference's stand-in natural image."""
+        p = np.empty((h, w))
+        st = self.lib.ref_phantom(w, h, _ptr(p))
+        if st:
+            raise CheckerError(st, "ref phantom")
+        return p
+
+    def psnr(self, a, b, peak=255.0) -> float:
+        a, b = _as_f64(a), _as_f64(b)
+        return float(self.lib.ref_psnr(_ptr(a), _ptr(b), a.shape[1], a.shape[0], peak))
+
+    def rmse(self, a, b) -> float:
+        a, b = _as_f64(a), _as_f64(b)
+        return float(self.lib.ref_rmse(_ptr(a), _ptr(b), a.shape[-1], a.size // a.shape[-1]))
 
     def set_max_threads(self, n: int) -> None:
         self.lib.ref_set_max_threads(n)

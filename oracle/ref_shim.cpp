@@ -15,7 +15,10 @@
 #include "osbf/filters2d.hpp"
 #include "osbf/filters3d.hpp"
 #include "osbf/io.hpp"
+#include "osbf/metrics.hpp"
 #include "osbf/parallel.hpp"
+#include "osbf/synth.hpp"
+#include "support/fixtures.hpp"
 
 namespace {
 
@@ -242,6 +245,57 @@ int ref_smooth_file(const char* in_path, const char* out_path, int filter, int r
     } catch (...) {
         return map_exception();
     }
+}
+
+// ---- acceptance-criterion inputs and metrics (acceptance.cpp:82-102,
+// :220-235, :293-319), generated by the reference's own synth / fixtures so
+// the GPU runs see the exact bytes the reference's checks use.
+
+// osbf::checkerboard (synth.hpp:52) + osbf::add_gaussian_noise (synth.hpp:94)
+int ref_checkerboard(int w, int h, int cell, double lo, double hi, double sigma,
+                     unsigned long long seed, double* clean, double* noisy) {
+    try {
+        const auto c = osbf::checkerboard(w, h, cell, lo, hi);
+        const auto n = osbf::add_gaussian_noise(c, {sigma, seed});
+        std::memcpy(clean, c.samples().data(), sizeof(double) * c.size());
+        std::memcpy(noisy, n.samples().data(), sizeof(double) * n.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// osbf::step_volume (synth.hpp:81) + add_gaussian_noise (synth.hpp:106)
+int ref_step_volume(int w, int h, int d, int edge, double lo, double hi, double sigma,
+                    unsigned long long seed, double* clean, double* noisy) {
+    try {
+        const auto c = osbf::step_volume(w, h, d, edge, lo, hi);
+        const auto n = osbf::add_gaussian_noise(c, {sigma, seed});
+        std::memcpy(clean, c.samples().data(), sizeof(double) * c.size());
+        std::memcpy(noisy, n.samples().data(), sizeof(double) * n.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// fixtures::phantom (tests/support/fixtures.hpp:36), the stand-in natural image
+int ref_phantom(int w, int h, double* out) {
+    try {
+        const auto p = fixtures::phantom(w, h);
+        std::memcpy(out, p.samples().data(), sizeof(double) * p.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// osbf::psnr / osbf::rmse (metrics.hpp:37-53)
+double ref_psnr(const double* a, const double* b, int w, int h, double peak) {
+    return osbf::psnr(to_plane(a, w, h), to_plane(b, w, h), peak);
+}
+double ref_rmse(const double* a, const double* b, int w, int h) {
+    return osbf::rmse(to_plane(a, w, h), to_plane(b, w, h));
 }
 
 }  // extern "C"

@@ -210,7 +210,7 @@ class Context:
             ret = out.view(src.shape)
         else:
             ret = out
-            out = out.view(batch, h, w)
+            out = _check_out(out, x, (batch, h, w))
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         _check(self._lib.osbf_gpu_iterate(
@@ -245,6 +245,10 @@ class Context:
         d, h, w = vol.shape
         if out is None:
             out = torch.empty_like(vol)
+        else:
+            out = _check_out(out, vol, (d, h, w))
+            if not out.is_contiguous():
+                raise InvalidArgument("out volume must be contiguous")
         if stream is None:
             stream = torch.cuda.current_stream(vol.device).cuda_stream
         _check(getattr(self._lib, fn)(self.handle, ctypes.c_void_p(vol.data_ptr()),
@@ -284,7 +288,7 @@ class Context:
             ret = out.view(src.shape)
         else:
             ret = out
-            out = out.view(batch, h, w)
+            out = _check_out(out, x, (batch, h, w))
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         _check(getattr(self._lib, fn)(
@@ -337,6 +341,12 @@ class Context:
             raise InvalidArgument("step_band expects 2-D row-major tensors")
         if out.dtype != torch.float64:
             raise InvalidArgument("band output must be float64")
+        if out.device != src.device:
+            raise InvalidArgument("band output must be on the input's device")
+        if out.shape[0] < out_rows or out.shape[1] != src.shape[1]:
+            raise InvalidArgument("band output must hold out_rows rows of the input's width")
+        if in_row0 > out_row0 or in_row0 + src.shape[0] < out_row0 + out_rows:
+            raise InvalidArgument("band input rows must cover the output rows")
         if stream is None:
             stream = torch.cuda.current_stream(src.device).cuda_stream
         pitch = 0
@@ -480,6 +490,25 @@ def _dtype_code(t) -> int:
     if code is None:
         raise InvalidArgument(f"unsupported dtype {t.dtype}")
     return code
+
+
+def _check_out(out, like, shape):
+    """A caller-supplied output: float64, on the input's device, of the
+    expected shape (any leading view of it), rows contiguous."""
+    import torch
+
+    if out.dtype != torch.float64:
+        raise InvalidArgument("out must be float64")
+    if not out.is_cuda or out.device != like.device:
+        raise InvalidArgument("out must be a CUDA tensor on the input's device")
+    if out.numel() != int(np.prod(shape)) or tuple(out.shape)[-2:] != tuple(shape)[-2:]:
+        raise InvalidArgument(f"out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.stride(-1) != 1:
+        raise InvalidArgument("out rows must be contiguous (stride(-1) == 1)")
+    if out.dim() == 3 and out.stride(0) < out.shape[1] * out.stride(1):
+        raise InvalidArgument("out planes overlap")
+    v = out.view(*shape) if out.dim() != len(shape) else out
+    return v
 
 
 def _as_batch(src):

@@ -94,6 +94,11 @@ struct osbf_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host entry points: copy overlap
     cudaStream_t capture = nullptr;                      // CUDA-graph capture stream
     std::vector<GraphEntry> graphs;                      // small LRU of replayable calls
+    // Scratch ordering across caller streams: the stream the last device call
+    // ran on, and an event recorded on it when a call switches streams.
+    cudaStream_t last_stream = nullptr;
+    bool have_last = false;
+    cudaEvent_t switch_ev = nullptr;
     void drop_graphs() {
         for (auto& gph : graphs)
             if (gph.exec) cudaGraphExecDestroy(gph.exec);
@@ -142,7 +147,24 @@ osbf_status check_mode(osbf_mode m) {
 // NULL is the CUDA default stream (standard cudaStream_t semantics), so work
 // is ordered with e.g. PyTorch's default stream.  The context's own stream is
 // used only by the host-buffer entry points.
-cudaStream_t pick_stream(osbf_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
+//
+// The context's scratch (ping/pong planes, exact-mode workspace, graphs) is
+// shared by every call, so calls issued on different streams must not
+// overlap: when a call arrives on a stream other than the previous call's,
+// the new stream first waits for everything already enqueued on the old one.
+cudaStream_t pick_stream(osbf_ctx* ctx, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ctx->have_last && ctx->last_stream != s) {
+        if (!ctx->switch_ev) cudaEventCreateWithFlags(&ctx->switch_ev, cudaEventDisableTiming);
+        if (ctx->switch_ev && cudaEventRecord(ctx->switch_ev, ctx->last_stream) == cudaSuccess)
+            cudaStreamWaitEvent(s, ctx->switch_ev, 0);
+        else
+            cudaGetLastError();  // old stream gone: its work was synchronized by its owner
+    }
+    ctx->last_stream = s;
+    ctx->have_last = true;
+    return s;
+}
 
 // Temporal blocking (two fast passes per launch) is opt-in per context
 // (osbf_gpu_ctx_set_temporal_blocking) or process-wide with OSBF_GPU_TB2=1.
@@ -190,13 +212,15 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
 // Copy/convert kernel: typed batch -> fp64 batch.
 template <typename T>
 __global__ void convert_kernel(const T* __restrict__ in, size_t ip, size_t ipl,
-                               double* __restrict__ out, size_t op, size_t opl, int W, int H) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
-    const int b = blockIdx.z;
-    if (x >= W) return;
-    out[b * opl + static_cast<size_t>(y) * op + x] =
-        static_cast<double>(in[b * ipl + static_cast<size_t>(y) * ip + x]);
+                               double* __restrict__ out, size_t op, size_t opl, int W, int H,
+                               int B) {
+    // grid-stride over rows of all planes (no 65535 limit on rows or planes)
+    const size_t rows = static_cast<size_t>(H) * B;
+    for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const size_t b = r / H, y = r % H;
+        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x)
+            out[b * opl + y * op + x] = static_cast<double>(in[b * ipl + y * ip + x]);
+    }
 }
 
 }  // namespace
@@ -211,20 +235,26 @@ const char* fast_kernel_override() { return g_fast_override.load(std::memory_ord
 
 cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t op,
                            size_t opl, cudaStream_t s, LaunchCounter& lc) {
-    dim3 grid((g.width + 255) / 256, g.height, g.batch);
+    const size_t rows = static_cast<size_t>(g.height) * g.batch;
+    dim3 grid(static_cast<unsigned>(std::min((g.width + 255) / 256, 64)),
+              static_cast<unsigned>(std::min<size_t>(rows, 65535)), 1);
     ++lc.launches;
+    note_kernel("convert_to_f64");
     switch (in.dtype) {
         case OSBF_U8:
             convert_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(in.base), in.pitch,
-                                                in.plane, out, op, opl, g.width, g.height);
+                                                in.plane, out, op, opl, g.width, g.height,
+                                                g.batch);
             break;
         case OSBF_F32:
             convert_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(in.base), in.pitch,
-                                                in.plane, out, op, opl, g.width, g.height);
+                                                in.plane, out, op, opl, g.width, g.height,
+                                                g.batch);
             break;
         default:
             convert_kernel<<<grid, 256, 0, s>>>(static_cast<const double*>(in.base), in.pitch,
-                                                in.plane, out, op, opl, g.width, g.height);
+                                                in.plane, out, op, opl, g.width, g.height,
+                                                g.batch);
             break;
     }
     return cudaGetLastError();
@@ -398,6 +428,7 @@ osbf_status osbf_gpu_ctx_create(int device, osbf_ctx** out) {
 osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx) {
     if (!ctx) return OSBF_OK;
     cudaSetDevice(ctx->device);
+    if (ctx->switch_ev) cudaEventDestroy(ctx->switch_ev);
     cudaStreamSynchronize(ctx->stream);
     ctx->ping.release();
     ctx->pong.release();
@@ -648,7 +679,7 @@ osbf_status filter3d_host(osbf_ctx* ctx, bool osbf3, const double* h_in, double*
     const size_t n = static_cast<size_t>(width) * height * depth;
     OSBF_CUDA(ctx->host_in.ensure(n * sizeof(double)), "alloc input");
     OSBF_CUDA(ctx->host_out.ensure(n * sizeof(double)), "alloc output");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * sizeof(double), cudaMemcpyHostToDevice, s),
               "H2D");
     osbf_status st = filter3d(ctx, osbf3, ctx->host_in.as<double>(), ctx->host_out.as<double>(),
@@ -692,7 +723,7 @@ osbf_status osbf_gpu_svt_host(osbf_ctx* ctx, const double* h_in, int width, int 
     OSBF_CUDA(ctx->host_in.ensure(n * sizeof(double)), "alloc input");
     OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc rows");
     OSBF_CUDA(ctx->host_out.ensure(nt * sizeof(double)), "alloc table");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, n * sizeof(double), cudaMemcpyHostToDevice, s),
               "H2D");
     OSBF_CUDA(osbf_gpu::svt_build(ctx->host_in.as<double>(), width, height, depth,
@@ -827,7 +858,7 @@ osbf_status host_batch(osbf_ctx* ctx, osbf_dtype in_dtype, const void* h_in, dou
     const size_t n = static_cast<size_t>(width) * height * batch;
     OSBF_CUDA(ctx->host_in.ensure(n * dtype_size(in_dtype)), "alloc input");
     OSBF_CUDA(ctx->host_out.ensure(n * sizeof(double)), "alloc output");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     const size_t plane = static_cast<size_t>(width) * height;
     const size_t in_bytes = plane * dtype_size(in_dtype);
     const char* hin = static_cast<const char*>(h_in);
@@ -986,7 +1017,7 @@ osbf_status multichannel_host(osbf_ctx* ctx, const double* const* h_in, double* 
     const size_t plane = static_cast<size_t>(width) * height;
     OSBF_CUDA(ctx->host_in.ensure(plane * channels * sizeof(double)), "alloc input");
     OSBF_CUDA(ctx->host_out.ensure(plane * channels * sizeof(double)), "alloc output");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     double* din = ctx->host_in.as<double>();
     double* dout = ctx->host_out.as<double>();
     for (int c = 0; c < channels; ++c) {
@@ -1072,7 +1103,7 @@ osbf_status osbf_gpu_smooth_raster_host(osbf_ctx* ctx, const void* h_raster, int
     OSBF_CUDA(ctx->host_in.ensure(planes_off + (direct ? 0 : plane_bytes)), "alloc input");
     const size_t raster_off = plane * channels * sizeof(double);
     OSBF_CUDA(ctx->host_out.ensure(raster_off + out_bytes), "alloc output");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     char* in_base = static_cast<char*>(ctx->host_in.ptr);
     double* dout = ctx->host_out.as<double>();
     void* draster_out = static_cast<char*>(ctx->host_out.ptr) + raster_off;
@@ -1114,7 +1145,7 @@ osbf_status osbf_gpu_sat_host(osbf_ctx* ctx, const double* h_in, int width, int 
     const size_t ns = static_cast<size_t>(width + 1) * (height + 1);
     OSBF_CUDA(ctx->host_in.ensure(plane * sizeof(double)), "alloc input");
     OSBF_CUDA(ctx->host_out.ensure(ns * sizeof(double)), "alloc output");
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = pick_stream(ctx, ctx->stream);
     OSBF_CUDA(cudaMemcpyAsync(ctx->host_in.ptr, h_in, plane * sizeof(double), cudaMemcpyHostToDevice,
                               s),
               "H2D");

@@ -61,6 +61,7 @@ constexpr int kUnrollRadius = 4;  // full unroll (register ring) up to this radi
 struct Band {
     int h_img;   // image height: windows clip at [0, h_img)
     int y_in0;   // global row of input buffer row 0
+    int in_rows; // rows held by the input buffer: [y_in0, y_in0 + in_rows)
     int y_out0;  // global row of output buffer row 0 (first output row)
     int y_end;   // one past the last output row (global)
     double* push_up;  // fused halo push (see Geometry); null = none
@@ -69,7 +70,7 @@ struct Band {
     long long push_pitch;
 };
 inline Band band_of(const Geometry& g) {
-    return Band{g.img_h(),  g.in_row0,  g.out_row0,    g.out_row0 + g.height,
+    return Band{g.img_h(),  g.in_row0,  g.in_h(),  g.out_row0,    g.out_row0 + g.height,
                 g.push_up,  g.push_dn,  g.push_rows,   static_cast<long long>(g.push_pitch)};
 }
 
@@ -133,7 +134,10 @@ __device__ __forceinline__ void stage_tile(const T* __restrict__ src, size_t pit
     constexpr int CHUNKS = (Ly::LWU + 31) / 32;
     for (int j = warp; j < Ly::LH; j += NT / 32) {
         const int gy = Y0 - R + j;  // global row; buffer row gy - y_in0
-        const bool row_in = !BORDER || (gy >= 0 && gy < band.h_img);
+        // rows outside the image read as zero; so do rows outside the caller's
+        // band buffer (they are only ever outside the windows' image part)
+        const bool row_in = !BORDER || (gy >= 0 && gy < band.h_img && gy >= band.y_in0 &&
+                                        gy < band.y_in0 + band.in_rows);
         const T* rowp = src + static_cast<size_t>(row_in ? gy - band.y_in0 : 0) * pitch;
 #pragma unroll
         for (int c = 0; c < CHUNKS; ++c) {

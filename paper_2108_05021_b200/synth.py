@@ -132,10 +132,7 @@ def make_input(name: str, seed: int | None = None, shrink: int = 1) -> np.ndarra
         batch = max(1, cfg.batch // shrink)
         out = np.empty((batch, h, w), dtype=np.float32)
         for i in range(batch):
-            rng = np.random.default_rng(1000 + i if seed is None else seed + i)
-            base = rect_mosaic(h, w, rng, size=(8, max(9, 256 // shrink))) if i % 2 == 0 else \
-                polygon_mosaic(h, w, rng, radii=(20.0 / shrink, 270.0 / shrink))[0]
-            out[i] = add_noise_f32(base, 0.05, rng)
+            out[i] = c4_plane(i, seed=seed, shrink=shrink)
         return out
     if name == "C5":
         rng = np.random.default_rng(5 if seed is None else seed)
@@ -143,6 +140,16 @@ def make_input(name: str, seed: int | None = None, shrink: int = 1) -> np.ndarra
         base = rect_mosaic(h, w, rng, n_rects=n, size=(16, 512))
         return add_noise_f32(base, 0.05, rng)[None]
     raise KeyError(name)
+
+
+def c4_plane(i: int, seed: int | None = None, shrink: int = 1) -> np.ndarray:
+    """Plane ``i`` of C4 alone (seed 1000 + i): a rectangle mosaic for even
+    ``i``, a polygon mosaic for odd ``i``, + N(0, 0.05^2), float32."""
+    h, w = CONFIGS["C4"].height // shrink, CONFIGS["C4"].width // shrink
+    rng = np.random.default_rng(1000 + i if seed is None else seed + i)
+    base = rect_mosaic(h, w, rng, size=(8, max(9, 256 // shrink))) if i % 2 == 0 else \
+        polygon_mosaic(h, w, rng, radii=(20.0 / shrink, 270.0 / shrink))[0]
+    return add_noise_f32(base, 0.05, rng)
 
 
 def make_c5_on_device(height: int = 32768, width: int = 32768, seed: int = 5, device="cuda"):

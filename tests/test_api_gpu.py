@@ -127,3 +127,73 @@ def test_fast_mode_large_radius_runs_exact_kernels(ctx, oracle_lib):
     p = np.random.default_rng(3).random((90, 70)) * 255
     got = ctx.iterate(torch.from_numpy(p).cuda(), 23, 2, mode="fast").cpu().numpy()
     assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 23, 2)))
+
+
+def test_out_argument_is_validated(ctx):
+    """A caller-supplied ``out`` must be float64, on the input's device, of
+    the input's shape, with contiguous rows (no silent 8-byte writes into a
+    smaller buffer)."""
+    import torch
+
+    import paper_2108_05021_b200 as ob
+
+    x = torch.rand((2, 40, 48), dtype=torch.float64, device="cuda")
+    for bad in (torch.empty((2, 40, 48), dtype=torch.float32, device="cuda"),
+                torch.empty((2, 40, 47), dtype=torch.float64, device="cuda"),
+                torch.empty((2, 48, 40), dtype=torch.float64, device="cuda"),
+                torch.empty((2, 40, 96), dtype=torch.float64, device="cuda")[:, :, ::2],
+                torch.empty((2, 40, 48), dtype=torch.float64)):
+        for fn in (lambda o: ctx.iterate(x, 2, 1, mode="fast", out=o),
+                   lambda o: ctx.box_filter(x, 2, 1, out=o),
+                   lambda o: ctx.fast_osbf(x, 2, 1, out=o)):
+            with pytest.raises(ob.InvalidArgument):
+                fn(bad)
+    good = torch.empty((2, 40, 48), dtype=torch.float64, device="cuda")
+    ctx.iterate(x, 2, 1, mode="fast", out=good)
+    vol = torch.rand((6, 7, 8), dtype=torch.float64, device="cuda")
+    with pytest.raises(ob.InvalidArgument):
+        ctx.osbf_3d(vol, 1, 1, out=torch.empty((6, 7, 9), dtype=torch.float64, device="cuda"))
+    band_src = torch.rand((30, 48), dtype=torch.float64, device="cuda")
+    with pytest.raises(ob.InvalidArgument):  # out smaller than out_rows
+        ctx.step_band(band_src, 0, torch.empty((10, 48), dtype=torch.float64, device="cuda"),
+                      0, 20, 30, 2)
+
+
+def test_calls_on_different_streams_are_ordered(ctx, oracle_lib):
+    """Calls issued on different streams share the context's scratch; the
+    context orders them, so alternating streams gives the same results as
+    one stream."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    planes = [rng.random((300, 500)) for _ in range(4)]
+    want = [oracle_lib.osbf(p, 3, 4) for p in planes]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    xs = [torch.from_numpy(p).cuda() for p in planes]
+    torch.cuda.synchronize()
+    outs = []
+    for i, x in enumerate(xs):
+        with torch.cuda.stream(streams[i % 2]):
+            outs.append(ctx.iterate(x, 3, 4, mode="exact"))
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want):
+        assert np.array_equal(bits(o.cpu().numpy()), bits(w))
+
+
+@pytest.mark.parametrize("w", [301, 77])
+def test_band_pass_odd_width_unaligned_cuts(ctx, oracle_lib, w):
+    """Row bands on layouts TMA cannot describe (odd fp64 widths: the
+    two-phase tile kernel) with unaligned cuts: the last partial tile of a
+    band must not read past the caller's band buffer, and the result equals
+    the whole-image pass."""
+    import torch
+
+    r, H = 3, 203
+    p = torch.from_numpy(np.random.default_rng(w).random((H, w))).cuda()
+    whole = ctx.iterate(p, r, 1, mode="fast")
+    out = torch.empty((H, w), dtype=torch.float64, device="cuda")
+    for a, b in ((0, 61), (61, 130), (130, H)):
+        i0, i1 = max(0, a - r), min(H, b + r)
+        src = p[i0:i1].clone()  # a tight buffer: nothing past its last row
+        ctx.step_band(src, i0, out[a:b], a, b - a, H, r)
+    assert float((out - whole).abs().max()) <= 1e-9
