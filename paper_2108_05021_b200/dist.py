@@ -25,7 +25,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-TILE_ROWS = 64  # fast-kernel tile height; band starts aligned to it
+TILE_ROWS = 128  # fast-kernel tile height (r = 3, 4); band starts aligned to it
 
 
 def shard_batch(batch: int, world: int, rank: int) -> tuple[int, int]:

@@ -16,7 +16,7 @@ def test_bench_defaults(monkeypatch):
     monkeypatch.setattr(sys, "argv", ["bench.py"])
     a = bench.parse()
     assert a.gpus == 1 and a.warmup >= 3 and 1 <= a.steps <= 100
-    assert a.impl == "ours" and a.workload == "C4" and a.mode == "fast"
+    assert a.impl == "ours" and a.workload == "C5" and a.mode == "fast"
     monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference", "--gpus", "2"])
     a = bench.parse()
     assert a.impl == "reference" and a.gpus == 2
