@@ -613,6 +613,206 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
 }
 
 // ---------------------------------------------------------------------------
+// Two columns per thread (r <= kTmaRadius): the TMA-staged tile of
+// fast_tma_step, but each thread walks the adjacent columns x0, x0 + 1 of its
+// segment.  Their windows share 2R of their 2R + 2 samples per row, loaded as
+// R + 1 aligned pairs (one 16-byte shared load per pair for fp64): per pixel
+// and row (R+1)/2 loads instead of 2R + 1, and the arms of x0 + 1 follow from
+// those of x0 with two adds each.  Outputs leave as 16-byte pair stores.
+template <int R, typename T>
+struct T2Lay {
+    static constexpr int TW2 = 64;             // columns per tile (32 lanes x 2)
+    static constexpr int NSB2 = 4;             // row segments (warps) per tile
+    static constexpr int NT2 = 32 * NSB2;
+    static constexpr int THT = R <= 2 ? 64 : 128;
+    static constexpr int SEGT = THT / NSB2;
+    static constexpr int LH = THT + 2 * R;
+    static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
+    static constexpr int RA = (R + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int XOFF = RA - R;        // smem column of image column X0 - R
+    static constexpr bool ODD = (XOFF & 1) != 0;  // pairs start one sample later
+    static constexpr int BW = (TW2 + RA + R + 1 + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
+    static constexpr int NRT = 2 * R + 2;
+    static constexpr size_t SMEM = TILE_BYTES + 128;
+    static constexpr int MINB = 2;
+};
+
+template <typename T>
+struct Pair;
+template <>
+struct Pair<double> {
+    using V = double2;
+};
+template <>
+struct Pair<float> {
+    using V = float2;
+};
+template <>
+struct Pair<uint8_t> {
+    using V = uchar2;
+};
+
+template <int R, typename T, bool EXACT_DIV, bool BORDER, bool VEC_OUT>
+__device__ __forceinline__ void pair_walk(const T* __restrict__ Us, int X0, int Y0, int W,
+                                          const Band& band, double* __restrict__ outp,
+                                          size_t out_pitch, const double* __restrict__ rtab) {
+    using Ly = T2Lay<R, T>;
+    using PV = typename Pair<T>::V;
+    const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
+    const int gx0 = X0 + 2 * lane;  // columns gx0, gx0 + 1
+    if (BORDER && gx0 >= W) return;
+    const bool has1 = !BORDER || gx0 + 1 < W;
+    ColFactors cf0{0.0, 0.0, 0.0}, cf1{0.0, 0.0, 0.0};
+    if (BORDER) {
+        int ncl = min(gx0, R) + 1, ncr = min(W - 1 - gx0, R) + 1;
+        cf0 = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+        ncl = min(gx0 + 1, R) + 1;
+        ncr = max(min(W - 2 - gx0, R), 0) + 1;
+        cf1 = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    const int y0 = s * Ly::SEGT;
+    // image (gx0 - R + i, Y0 + y0 + j - R) = row[j * BW + i], i in [0, 2R + 2)
+    const T* __restrict__ row = Us + y0 * Ly::BW + 2 * lane + Ly::XOFF;
+    const int H = band.h_img;
+    double* o = outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx0;
+    constexpr int NJ = Ly::SEGT + 2 * R;
+    double P1a[NJ + 1], P2a[NJ + 1], Qa[NJ + 1], Ua[NJ];
+    double P1b[NJ + 1], P2b[NJ + 1], Qb[NJ + 1], Ub[NJ];
+    P1a[0] = P2a[0] = Qa[0] = P1b[0] = P2b[0] = Qb[0] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        double v[2 * R + 2];
+        const T* rj = row + j * Ly::BW;
+        if constexpr (Ly::ODD) {
+            v[0] = to_f64(rj[0]);
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const PV p = *reinterpret_cast<const PV*>(rj + 1 + 2 * i);
+                v[1 + 2 * i] = to_f64(p.x);
+                v[2 + 2 * i] = to_f64(p.y);
+            }
+            v[2 * R + 1] = to_f64(rj[2 * R + 1]);
+        } else {
+#pragma unroll
+            for (int i = 0; i <= R; ++i) {
+                const PV p = *reinterpret_cast<const PV*>(rj + 2 * i);
+                v[2 * i] = to_f64(p.x);
+                v[2 * i + 1] = to_f64(p.y);
+            }
+        }
+        // column a = gx0: arms over v[0..R] and v[R..2R]; column b = gx0 + 1
+        // slides them by one sample
+        double a1 = v[0], a2 = v[R];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) {
+            a1 += v[i];
+            a2 += v[R + i];
+        }
+        const double b1 = a1 + (v[R + 1] - v[0]);
+        const double b2 = a2 + (v[2 * R + 1] - v[R]);
+        const double ua = v[R], ub = v[R + 1];
+        Ua[j] = ua;
+        Ub[j] = ub;
+        P1a[j + 1] = P1a[j] + a1;
+        P2a[j + 1] = P2a[j] + a2;
+        Qa[j + 1] = Qa[j] + ((a1 + a2) - ua);
+        P1b[j + 1] = P1b[j] + b1;
+        P2b[j + 1] = P2b[j] + b2;
+        Qb[j + 1] = Qb[j] + ((b1 + b2) - ub);
+        const int y = j - 2 * R;
+        if (y >= 0) {
+            const int gy = Y0 + y0 + y;
+            if (BORDER && gy >= band.y_end) break;
+            const double Sa[8] = {P1a[y + 2 * R + 1] - P1a[y + R], P2a[y + 2 * R + 1] - P2a[y + R],
+                                  P2a[y + R + 1] - P2a[y],         P1a[y + R + 1] - P1a[y],
+                                  P1a[y + 2 * R + 1] - P1a[y],     P2a[y + 2 * R + 1] - P2a[y],
+                                  Qa[y + 2 * R + 1] - Qa[y + R],   Qa[y + R + 1] - Qa[y]};
+            const double Sb[8] = {P1b[y + 2 * R + 1] - P1b[y + R], P2b[y + 2 * R + 1] - P2b[y + R],
+                                  P2b[y + R + 1] - P2b[y],         P1b[y + R + 1] - P1b[y],
+                                  P1b[y + 2 * R + 1] - P1b[y],     P2b[y + 2 * R + 1] - P2b[y],
+                                  Qb[y + 2 * R + 1] - Qb[y + R],   Qb[y + R + 1] - Qb[y]};
+            double va, vb = 0.0, tmp;
+            va = select_store<R, EXACT_DIV, BORDER, false>(Sa, Ua[y + R], gx0, gy, W, H, 0, &tmp,
+                                                           nullptr, nullptr, cf0, rtab);
+            if (!BORDER || has1)
+                vb = select_store<R, EXACT_DIV, BORDER, false>(Sb, Ub[y + R], gx0 + 1, gy, W, H, 0,
+                                                               &tmp, nullptr, nullptr, cf1, rtab);
+            if constexpr (VEC_OUT && !BORDER) {
+                *reinterpret_cast<double2*>(o) = make_double2(va, vb);
+            } else {
+                o[0] = va;
+                if (!BORDER || has1) o[1] = vb;
+            }
+            o += out_pitch;
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV, bool VEC_OUT>
+__global__ void __launch_bounds__(T2Lay<R, T>::NT2, T2Lay<R, T>::MINB)
+    fast_tma_pair(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+                  size_t out_pitch, size_t out_plane, int W, Band band) {
+    using Ly = T2Lay<R, T>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ double rtab[Ly::NRT];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    T* Us = reinterpret_cast<T*>(smem_raw + ((128u - (base & 127u)) & 127u));
+    const int X0 = blockIdx.x * Ly::TW2, Y0 = band.y_out0 + blockIdx.y * Ly::THT, b = blockIdx.z;
+    if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
+    if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
+        tma::load_3d(Us, &tmap, X0 - Ly::RA, Y0 - R - band.y_in0, b, &bar);
+    }
+    tma::mbar_wait(&bar, 0);
+    double* outp = out + static_cast<size_t>(b) * out_plane;
+    if (X0 >= R && X0 + Ly::TW2 + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
+        Y0 + Ly::THT <= band.y_end)
+        pair_walk<R, T, EXACT_DIV, false, VEC_OUT>(Us, X0, Y0, W, band, outp, out_pitch, rtab);
+    else
+        pair_walk<R, T, EXACT_DIV, true, VEC_OUT>(Us, X0, Y0, W, band, outp, out_pitch, rtab);
+    if (band.push_rows) {  // row-band mode with the fused halo push
+        const int lane = threadIdx.x & 31, ya = Y0 + (threadIdx.x >> 5) * Ly::SEGT;
+        for (int c = 0; c < 2; ++c) {
+            const int gx = X0 + 2 * lane + c;
+            if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+cudaError_t launch_pair(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                        size_t opl, cudaStream_t s) {
+    using Ly = T2Lay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+        return cudaErrorNotSupported;
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0 && op % 2 == 0 &&
+                     (g.batch == 1 || opl % 2 == 0);
+    dim3 grid((g.width + Ly::TW2 - 1) / Ly::TW2, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
+    note_kernel("fast_tma_pair");
+    if (vec) {
+        static std::atomic<unsigned long long> done{0};
+        if (cudaError_t e = ensure_smem(fast_tma_pair<R, T, EXACT_DIV, true>, Ly::SMEM, done))
+            return e;
+        fast_tma_pair<R, T, EXACT_DIV, true><<<grid, Ly::NT2, Ly::SMEM, s>>>(
+            map, out, op, opl, g.width, band_of(g));
+    } else {
+        static std::atomic<unsigned long long> done{0};
+        if (cudaError_t e = ensure_smem(fast_tma_pair<R, T, EXACT_DIV, false>, Ly::SMEM, done))
+            return e;
+        fast_tma_pair<R, T, EXACT_DIV, false><<<grid, Ly::NT2, Ly::SMEM, s>>>(
+            map, out, op, opl, g.width, band_of(g));
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Persistent tile kernel (r <= kTmaRadius): the same per-tile computation as
 // fast_tma_step (bit-identical outputs), but a grid of #SMs x occupancy CTAs
 // walks the tiles round robin with two shared-memory tile buffers, so the TMA
@@ -803,6 +1003,17 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
     if constexpr (!DIAG) {
         if (fast_allowed("strip", false)) {
             const cudaError_t e = strip_launch_radius<R>(in, g, out, op, opl, s);
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R <= kTmaRadius && !DIAG) {
+        if (fast_allowed("pair", false)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_pair<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_pair<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_pair<R, double, false>(in, g, out, op, opl, s); break;
+            }
             if (e != cudaErrorNotSupported) return e;
         }
     }
