@@ -94,10 +94,12 @@ osbf_status osbf_gpu_ctx_destroy(osbf_ctx* ctx);
 osbf_status osbf_gpu_ctx_trim(osbf_ctx* ctx);
 /* Number of kernels this context has launched so far (instrumentation). */
 uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx);
-/* Fast mode temporal blocking: 2 = run two passes per launch (tile staged
- * with a 2r halo, intermediate kept in shared memory) where a two-pass
- * kernel exists (radius <= 2), 1 = one pass per launch (default).  Same
- * results either way up to the fast mode's fp64 rounding. */
+/* Fast mode temporal blocking (north-star K4): passes_per_launch = k in
+ * 2..4 runs k passes per launch over tiles staged with a k*r halo (the k-1
+ * intermediate planes live in shared memory, every pass clips its windows at
+ * the global image border), for radius <= 4; the HBM traffic per iteration
+ * drops k-fold.  1 = one pass per launch (default).  Results equal the
+ * single-pass ones up to the fast mode's fp64 rounding. */
 osbf_status osbf_gpu_ctx_set_temporal_blocking(osbf_ctx* ctx, int passes_per_launch);
 
 /* ---- device-resident entry points (throughput path) ---------------------- */

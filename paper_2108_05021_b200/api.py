@@ -195,7 +195,8 @@ class Context:
         return self._lib.osbf_gpu_last_kernel().decode()
 
     def set_temporal_blocking(self, passes_per_launch: int) -> None:
-        """Fast mode: 2 = two passes per launch (radius <= 2), 1 = default."""
+        """Fast mode temporal blocking: k = 2..4 passes per launch over tiles
+        with a k*r halo (radius <= 4); 1 = one pass per launch (default)."""
         _check(self._lib.osbf_gpu_ctx_set_temporal_blocking(self.handle, passes_per_launch))
 
     # -- device tensors -----------------------------------------------------

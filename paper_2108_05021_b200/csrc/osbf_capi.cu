@@ -90,7 +90,7 @@ struct osbf_ctx {
     DevBuf rowpfx, sat;        // exact-mode workspace
     DevBuf host_in, host_out;  // staging for the host entry points
     osbf_gpu::LaunchCounter lc;
-    int passes_per_launch = 1;  // fast mode temporal blocking: 1 or 2
+    int passes_per_launch = 1;  // fast mode temporal blocking: 1..4 passes per launch
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host entry points: copy overlap
     cudaStream_t capture = nullptr;                      // CUDA-graph capture stream
     std::vector<GraphEntry> graphs;                      // small LRU of replayable calls
@@ -166,14 +166,17 @@ cudaStream_t pick_stream(osbf_ctx* ctx, void* stream) {
     return s;
 }
 
-// Temporal blocking (two fast passes per launch) is opt-in per context
-// (osbf_gpu_ctx_set_temporal_blocking) or process-wide with OSBF_GPU_TB2=1.
-bool tb2_env() {
-    static const bool on = [] {
-        const char* v = std::getenv("OSBF_GPU_TB2");
-        return v && v[0] == '1';
+// Temporal blocking (k fast passes per launch, k = 2..4) is opt-in per
+// context (osbf_gpu_ctx_set_temporal_blocking) or process-wide with
+// OSBF_GPU_TB=k (OSBF_GPU_TB2=1 = k 2).
+int tb_env() {
+    static const int k = [] {
+        const char* v = std::getenv("OSBF_GPU_TB");
+        if (v && v[0] >= '2' && v[0] <= '4' && v[1] == 0) return v[0] - '0';
+        const char* v2 = std::getenv("OSBF_GPU_TB2");
+        return (v2 && v2[0] == '1') ? 2 : 1;
     }();
-    return on;
+    return k;
 }
 
 // One pass in the requested mode: src (typed view) -> dst (fp64).
@@ -265,9 +268,9 @@ namespace {
 
 // Jacobi ping-pong through context scratch (filters2d.hpp:94-97 / :112-152:
 // every iteration reads the previous plane and writes a fresh one); the last
-// launch writes d_out.  want(remaining) is the number of passes (1 or 2) the
+// launch writes d_out.  want(remaining) is the number of passes (1..4) the
 // next launch should run; run(src, dst, dst_pitch, dst_plane, n, &retry)
-// launches them, setting retry when n = 2 has no kernel (then one pass).
+// launches them, setting retry when n > 1 has no kernel (then one pass).
 template <typename Want, typename Run>
 osbf_status jacobi(osbf_ctx* ctx, const osbf_gpu::PlaneView& input, const osbf_gpu::Geometry& g,
                    int iterations, double* d_out, size_t out_pitch, size_t out_plane,
@@ -297,7 +300,7 @@ osbf_status jacobi(osbf_ctx* ctx, const osbf_gpu::PlaneView& input, const osbf_g
             }
             bool retry = false;
             const osbf_status st = run(src, dst, dp, dpl, n, &retry);
-            if (retry && n == 2) {
+            if (retry && n > 1) {
                 n = 1;
                 continue;
             }
@@ -464,8 +467,8 @@ uint64_t osbf_gpu_ctx_launch_count(const osbf_ctx* ctx) { return ctx ? ctx->lc.l
 
 osbf_status osbf_gpu_ctx_set_temporal_blocking(osbf_ctx* ctx, int passes_per_launch) {
     if (!ctx) return fail(OSBF_ERR_INVALID_ARGUMENT, "null context");
-    if (passes_per_launch != 1 && passes_per_launch != 2)
-        return fail(OSBF_ERR_INVALID_ARGUMENT, "passes_per_launch must be 1 or 2");
+    if (passes_per_launch < 1 || passes_per_launch > 4)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "passes_per_launch must be in 1..4");
     ctx->passes_per_launch = passes_per_launch;
     return OSBF_OK;
 }
@@ -502,16 +505,17 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
     }
     // Fast mode runs two passes per launch (temporal blocking) when enabled
     // and the radius has a two-pass kernel; otherwise one pass per launch.
-    const bool tb2 = mode == OSBF_MODE_FAST && (ctx->passes_per_launch == 2 || tb2_env());
+    const int tbk = mode != OSBF_MODE_FAST ? 1
+                    : (ctx->passes_per_launch > 1 ? ctx->passes_per_launch : tb_env());
     auto body = [&](cudaStream_t st_) {
         return jacobi(
             ctx, input, g, iterations, d_out, out_pitch, out_plane_stride, st_,
-            [&](int remaining) { return tb2 && remaining >= 2 ? 2 : 1; },
+            [&](int remaining) { return remaining < tbk ? remaining : tbk; },
             [&](const osbf_gpu::PlaneView& src, double* dst, size_t dp, size_t dpl, int n,
                 bool* retry) -> osbf_status {
-                if (n == 2) {
+                if (n > 1) {
                     const cudaError_t e =
-                        osbf_gpu::fast_step2(src, g, radius, dst, dp, dpl, st_, ctx->lc);
+                        osbf_gpu::fast_stepk(src, g, radius, n, dst, dp, dpl, st_, ctx->lc);
                     if (e == cudaErrorNotSupported) {
                         cudaGetLastError();
                         *retry = true;
@@ -529,7 +533,7 @@ osbf_status osbf_gpu_iterate(osbf_ctx* ctx, osbf_dtype in_dtype, const void* d_i
         static_cast<uintptr_t>(width), static_cast<uintptr_t>(height),
         static_cast<uintptr_t>(batch), static_cast<uintptr_t>(radius),
         static_cast<uintptr_t>(iterations), static_cast<uintptr_t>(mode),
-        static_cast<uintptr_t>(tb2)};
+        static_cast<uintptr_t>(tbk)};
     return run_graphed(ctx, key, s, body);
 }
 

@@ -270,7 +270,8 @@ template <typename L, bool SAFE>
 __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
                                              const double* __restrict__ U, int xs, int X0, int yb,
                                              int r_lo, int r_hi, int w_first, int n_w, int W,
-                                             int H, double* __restrict__ outp, size_t opitch) {
+                                             int H, double* __restrict__ outp, size_t opitch,
+                                             const double* __restrict__ rcp) {
     constexpr int R = L::RAD;
     const int lx = threadIdx.x & 31, grp = (threadIdx.x >> 5) - w_first;
     const int x = X0 + lx;
@@ -358,8 +359,9 @@ __device__ __forceinline__ void stencil_rows(const double* __restrict__ Cr,
                 const double A = rb[x1 + 1 - cbase], Bv = rb[x0 - cbase];
                 const double Cv = ra[x1 + 1 - cbase], D = ra[x0 - cbase];
                 const double s = __dadd_rn(__dsub_rn(__dsub_rn(A, Bv), Cv), D);
-                const double n = static_cast<double>((x1 - x0 + 1) * (y1 - y0 + 1));
-                const double a = div_by_count(s, n, __ddiv_rn(1.0, n));
+                const int ni = (x1 - x0 + 1) * (y1 - y0 + 1);
+                const double n = static_cast<double>(ni);
+                const double a = div_by_count(s, n, rcp[ni]);
                 const double d = fabs(__dsub_rn(a, u));
                 if (d < best_abs) {
                     best_abs = d;
@@ -400,6 +402,11 @@ __global__ void __launch_bounds__(NT, 2)
     double* outp = out + static_cast<size_t>(b) * oplane;
     const long long gbase = static_cast<long long>(b) * H;
     const int tid = threadIdx.x;
+    // RN(1/n) for every clipped window count (border pixels): one load
+    // instead of an IEEE division per window
+    __shared__ double rcp_tab[(2 * R + 1) * (R + 1) + 1];
+    for (int n = threadIdx.x; n <= (2 * R + 1) * (R + 1); n += blockDim.x)
+        rcp_tab[n] = n ? __ddiv_rn(1.0, static_cast<double>(n)) : 0.0;
     const int nbands = band_h > 0 ? (H + band_h - 1) / band_h : 1;
     const int band = CARRIES ? 0 : blockIdx.z;
     int y_out_lo = 0, y_out_hi = H, y_walk0 = 0, y_walk_end = H;
@@ -482,10 +489,10 @@ __global__ void __launch_bounds__(NT, 2)
         if (lo >= hi) return;
         if (safe)
             stencil_rows<L, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
-                                  opitch);
+                                  opitch, rcp_tab);
         else
             stencil_rows<L, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
-                                   opitch);
+                                   opitch, rcp_tab);
     };
     for (int k = 0; k < nblocks; ++k) {
         const int y0 = y_walk0 + k * BR;
@@ -583,6 +590,11 @@ __global__ void __launch_bounds__(NT, 2)
     double* outp = out + static_cast<size_t>(b) * oplane;
     const long long gbase = static_cast<long long>(b) * H;
     const int tid = threadIdx.x, warp = tid >> 5;
+    // RN(1/n) for every clipped window count (border pixels): one load
+    // instead of an IEEE division per window
+    __shared__ double rcp_tab[(2 * R + 1) * (R + 1) + 1];
+    for (int n = threadIdx.x; n <= (2 * R + 1) * (R + 1); n += blockDim.x)
+        rcp_tab[n] = n ? __ddiv_rn(1.0, static_cast<double>(n)) : 0.0;
     const int nbands = band_h > 0 ? (H + band_h - 1) / band_h : 1;
     const int band = blockIdx.z;
     int y_out_lo = 0, y_out_hi = H, y_walk0 = 0, y_walk_end = H;
@@ -637,10 +649,10 @@ __global__ void __launch_bounds__(NT, 2)
         if (lo >= hi) return;
         if (safe)
             stencil_rows<L, true>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
-                                  opitch);
+                                  opitch, rcp_tab);
         else
             stencil_rows<L, false>(Cr, U_of(j), xs, X0, yb, lo, hi, w_first, n_w, W, H, outp,
-                                   opitch);
+                                   opitch, rcp_tab);
     };
 
     double creg = 0.0;

@@ -68,20 +68,20 @@ cudaError_t fast_launch_radius(const PlaneView& in, const Geometry& g, double* o
                                cudaStream_t s);
 
 template <int R>
-cudaError_t fast_launch_radius2(const PlaneView& in, const Geometry& g, double* out,
+cudaError_t fast_launch_radiusk(const PlaneView& in, const Geometry& g, int k, double* out,
                                 size_t out_pitch, size_t out_plane, cudaStream_t s);
 
 namespace {
-using Launch2Fn = cudaError_t (*)(const PlaneView&, const Geometry&, double*, size_t, size_t,
-                                  cudaStream_t);
-constexpr Launch2Fn kByRadius2[kFastMaxRadius + 1] = {
+using LaunchKFn = cudaError_t (*)(const PlaneView&, const Geometry&, int, double*, size_t,
+                                  size_t, cudaStream_t);
+constexpr LaunchKFn kByRadiusK[kFastMaxRadius + 1] = {
     nullptr,
-    fast_launch_radius2<1>,  fast_launch_radius2<2>,  fast_launch_radius2<3>,
-    fast_launch_radius2<4>,  fast_launch_radius2<5>,  fast_launch_radius2<6>,
-    fast_launch_radius2<7>,  fast_launch_radius2<8>,  fast_launch_radius2<9>,
-    fast_launch_radius2<10>, fast_launch_radius2<11>, fast_launch_radius2<12>,
-    fast_launch_radius2<13>, fast_launch_radius2<14>, fast_launch_radius2<15>,
-    fast_launch_radius2<16>,
+    fast_launch_radiusk<1>,  fast_launch_radiusk<2>,  fast_launch_radiusk<3>,
+    fast_launch_radiusk<4>,  fast_launch_radiusk<5>,  fast_launch_radiusk<6>,
+    fast_launch_radiusk<7>,  fast_launch_radiusk<8>,  fast_launch_radiusk<9>,
+    fast_launch_radiusk<10>, fast_launch_radiusk<11>, fast_launch_radiusk<12>,
+    fast_launch_radiusk<13>, fast_launch_radiusk<14>, fast_launch_radiusk<15>,
+    fast_launch_radiusk<16>,
 };
 using LaunchFn = cudaError_t (*)(const PlaneView&, const Geometry&, double*, size_t, size_t,
                                  double*, uint8_t*, cudaStream_t);
@@ -105,10 +105,10 @@ cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double
     return kByRadius[radius](in, g, out, out_pitch, out_plane, means, sel, s);
 }
 
-cudaError_t fast_step2(const PlaneView& in, const Geometry& g, int radius, double* out,
+cudaError_t fast_stepk(const PlaneView& in, const Geometry& g, int radius, int k, double* out,
                        size_t out_pitch, size_t out_plane, cudaStream_t s, LaunchCounter& lc) {
     if (radius < 1 || radius > kFastMaxRadius) return cudaErrorNotSupported;
-    const cudaError_t e = kByRadius2[radius](in, g, out, out_pitch, out_plane, s);
+    const cudaError_t e = kByRadiusK[radius](in, g, k, out, out_pitch, out_plane, s);
     if (e == cudaSuccess) ++lc.launches;
     return e;
 }

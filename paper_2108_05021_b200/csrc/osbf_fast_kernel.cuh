@@ -74,6 +74,15 @@ inline Band band_of(const Geometry& g) {
                 g.push_up,  g.push_dn,  g.push_rows,   static_cast<long long>(g.push_pitch)};
 }
 
+// Tile-row order of a launch: in row-band mode with the fused halo push the
+// band's first and last tile rows run first (rows 0, n-1, 1, n-2, ...), so
+// the pushes into the neighbours' halos fly while the interior is computed.
+__device__ __forceinline__ int tile_row(const Band& bd) {
+    const int i = blockIdx.y, n = gridDim.y;
+    if (bd.push_rows == 0) return i;
+    return (i & 1) ? n - 1 - (i >> 1) : (i >> 1);
+}
+
 // Fused halo exchange: a band's first / last push_rows output rows are also
 // written straight into the neighbours' halo rows (peer memory over NVLink
 // when the ranks are GPUs), so no separate exchange step follows the pass.
@@ -565,7 +574,7 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : TVar<R, T, 
     __shared__ double rtab[Ly::NRT];
     const uint32_t base = tma::smem_u32(smem_raw);
     T* Us = reinterpret_cast<T*>(smem_raw + ((128u - (base & 127u)) & 127u));
-    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * Ly::THT, b = blockIdx.z;
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + tile_row(band) * Ly::THT, b = blockIdx.z;
     if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
     if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
     __syncthreads();
@@ -1087,36 +1096,44 @@ cudaError_t fast_launch_radius(const PlaneView& in, const Geometry& g, double* o
 }  // namespace osbf_gpu
 
 // ===========================================================================
-// Temporal blocking: two OSBF passes per HBM round trip (north-star K4).
+// Temporal blocking: K OSBF passes per HBM round trip (north-star K4),
+// K = 2..4, radius <= kTbRadius.
 //
-// The tile is staged with a 2R halo; pass 1 computes the intermediate plane
-// over the output tile plus an R halo into shared memory (exactly what a
-// separate pass would write to HBM: clipped counts at the global border,
-// zero outside the image so pass 2's sums see the same zero fill); pass 2
-// computes the output tile from it.  HBM traffic per iteration halves; the
-// extra work is the R-wide ring of intermediate pixels ((TW+2R)(TH+2R)/TW/TH).
+// The output tile is staged with a K*R halo; pass p (1..K-1) computes the
+// intermediate plane over the output tile plus a (K-p)*R halo into shared
+// memory (exactly what a separate pass would write to HBM: clipped counts at
+// the GLOBAL image border, zero outside the image so the next pass's sums see
+// the same zero fill); pass K computes the output tile from pass K-1.  HBM
+// traffic per iteration drops K-fold; the extra work is the shrinking halo
+// rings of intermediate pixels: sum_p (T + 2(K-p)R)^2 / (K T^2).
 namespace osbf_gpu {
 namespace fastk {
 
-template <int R, typename T>
-struct TB2Lay {
-    static constexpr int IW = TW + 2 * R;  // intermediate columns: [X0-R, X0+TW+R)
-    static constexpr int IH = TH + 2 * R;  // intermediate rows
-    static constexpr int IP = IW;          // intermediate pitch (doubles)
+constexpr int kTbRadius = 4;
+constexpr int kTbMaxPasses = 4;
+
+template <int R, typename T, int K>
+struct TBKLay {
+    static constexpr int TWK = 64, THK = 64;  // output tile
+    static constexpr int HALO = K * R;
     static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
-    static constexpr int RA2 = (2 * R + ALIGN - 1) / ALIGN * ALIGN;  // aligned 2R halo
-    static constexpr int XOFF = RA2 - 2 * R;
-    static constexpr int BW = (TW + RA2 + 2 * R + ALIGN - 1) / ALIGN * ALIGN;
-    static constexpr int LH = TH + 4 * R;
+    static constexpr int RAK = (HALO + ALIGN - 1) / ALIGN * ALIGN;  // aligned K*R halo
+    static constexpr int XOFF = RAK - HALO;
+    static constexpr int BW = (TWK + RAK + HALO + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int LH = THK + 2 * HALO;
     static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
-    static constexpr int NSEG1 = 4, NSEG2 = 4;
-    static constexpr int SEG1 = (IH + NSEG1 - 1) / NSEG1;  // pass-1 rows per segment
-    static constexpr int SEG2 = TH / NSEG2;
-    static constexpr int NT1 = IW * NSEG1, NT2 = TW * NSEG2;
-    static constexpr int NTT = ((NT1 > NT2 ? NT1 : NT2) + 31) / 32 * 32;
+    static constexpr int NSEG = 4;  // row segments per column in every pass
+    static constexpr int IW(int p) { return TWK + 2 * (K - p) * R; }  // pass p's width = height
+    // A walk of SEG rows reads SEG + 2R source rows even when its last
+    // segment is shorter: the intermediates carry PADR spare rows.
+    static constexpr int PADR = NSEG + 2;
+    static constexpr size_t IA = sizeof(double) * static_cast<size_t>(IW(1)) * (IW(1) + PADR);
+    static constexpr size_t IB =
+        K >= 3 ? sizeof(double) * static_cast<size_t>(IW(2)) * (IW(2) + PADR) : 0;
+    static constexpr int NTT = (IW(1) * NSEG + 31) / 32 * 32;
     static constexpr int NRT = 2 * R + 2;
-    static constexpr size_t I_BYTES = sizeof(double) * static_cast<size_t>(IH) * IP;
-    static constexpr size_t SMEM = 128 + ((TILE_BYTES + 15) / 16) * 16 + I_BYTES;
+    static constexpr size_t SMEM = 128 + ((TILE_BYTES + 15) / 16) * 16 + IA + IB;
+    static constexpr int MINB = (SMEM + 1024) * 2 <= 227 * 1024 ? 2 : 1;
 };
 
 // One column walk (prefix-sum formulation, see direct_walk): source rows
@@ -1156,23 +1173,18 @@ __device__ __forceinline__ void tb_walk(const S* __restrict__ col, int pitch, in
         const int y = j - 2 * R;
         if (y >= 0 && y < nrows) {
             const int gy = gy0 + y;
+            const double S8[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                  P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                  P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                  Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
             if (TO_SMEM) {
-                if (!BORDER || (col_in && gy >= 0 && gy < H)) {
-                    const double S8[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
-                                          P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
-                                          P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
-                                          Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+                if (!BORDER || (col_in && gy >= 0 && gy < H))
                     select_store<R, EXACT_DIV, BORDER, false>(S8, Uc[y + R], gx, gy, W, H, 0, o,
                                                               nullptr, nullptr, cf, rtab);
-                } else {
+                else
                     *o = 0.0;
-                }
             } else {
                 if (BORDER && gy >= band.y_end) break;
-                const double S8[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
-                                      P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
-                                      P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
-                                      Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
                 select_store<R, EXACT_DIV, BORDER, false>(S8, Uc[y + R], gx, gy, W, H, 0, o,
                                                           nullptr, nullptr, cf, rtab);
             }
@@ -1181,103 +1193,152 @@ __device__ __forceinline__ void tb_walk(const S* __restrict__ col, int pitch, in
     }
 }
 
-template <int R, typename T, bool EXACT1>
-__global__ void __launch_bounds__(TB2Lay<R, T>::NTT, 2)
-    fast_tma_step2(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+// Pass P of K (P < K) into shared memory: columns / rows [X0, Y0) - (K-P)R,
+// width = height = IW(P); the source is the staged tile (P = 1) or pass P-1.
+template <int R, typename T, int K, int P, bool EXACT1>
+__device__ __forceinline__ void tbk_smem_pass(const void* src, double* dst, int X0, int Y0,
+                                              int W, const Band& band, bool interior,
+                                              const double* rtab) {
+    using Ly = TBKLay<R, T, K>;
+    using S = std::conditional_t<P == 1, T, double>;
+    constexpr int IWp = Ly::IW(P);
+    constexpr int SPITCH = P == 1 ? Ly::BW : Ly::IW(P - 1);
+    constexpr int SOFF = P == 1 ? Ly::XOFF : 0;
+    constexpr int SEGp = (IWp + Ly::NSEG - 1) / Ly::NSEG;
+    constexpr bool EX = P == 1 && EXACT1;
+    const int tid = threadIdx.x;
+    if (tid >= IWp * Ly::NSEG) return;
+    const int xi = tid % IWp, s = tid / IWp;
+    const int yi0 = s * SEGp;
+    const int nrows = min(SEGp, IWp - yi0);
+    if (nrows <= 0) return;
+    const S* col = static_cast<const S*>(src) + yi0 * SPITCH + xi + SOFF;
+    double* o = dst + yi0 * IWp + xi;
+    const int gx = X0 - (K - P) * R + xi, gy0 = Y0 - (K - P) * R + yi0;
+    if (interior)
+        tb_walk<R, S, EX, false, true, SEGp>(col, SPITCH, nrows, gx, gy0, W, band, o, IWp, rtab);
+    else
+        tb_walk<R, S, EX, true, true, SEGp>(col, SPITCH, nrows, gx, gy0, W, band, o, IWp, rtab);
+}
+
+template <int R, typename T, int K, bool EXACT1>
+__global__ void __launch_bounds__(TBKLay<R, T, K>::NTT, TBKLay<R, T, K>::MINB)
+    fast_tma_stepk(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
                    size_t out_pitch, size_t out_plane, int W, Band band) {
-    using Ly = TB2Lay<R, T>;
+    using Ly = TBKLay<R, T, K>;
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ double rtab[Ly::NRT];
     const uint32_t base = tma::smem_u32(smem_raw);
     unsigned char* aligned = smem_raw + ((128u - (base & 127u)) & 127u);
     T* Us = reinterpret_cast<T*>(aligned);
-    double* Is = reinterpret_cast<double*>(aligned + ((Ly::TILE_BYTES + 15) / 16) * 16);
-    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + blockIdx.y * TH, b = blockIdx.z;
+    double* IA = reinterpret_cast<double*>(aligned + ((Ly::TILE_BYTES + 15) / 16) * 16);
+    double* IB = IA + Ly::IA / sizeof(double);
+    const int X0 = blockIdx.x * Ly::TWK, Y0 = band.y_out0 + tile_row(band) * Ly::THK;
+    const int b = blockIdx.z;
     const int tid = threadIdx.x;
     if (tid == 0) tma::mbar_init(&bar, 1);
     if (tid < Ly::NRT) rtab[tid] = tid ? 1.0 / tid : 0.0;
     __syncthreads();
     if (tid == 0) {
         tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
-        tma::load_3d(Us, &tmap, X0 - Ly::RA2, Y0 - 2 * R - band.y_in0, b, &bar);
+        tma::load_3d(Us, &tmap, X0 - Ly::RAK, Y0 - Ly::HALO - band.y_in0, b, &bar);
     }
     tma::mbar_wait(&bar, 0);
     // interior: every intermediate and output position inside the image
-    const bool interior = X0 >= 2 * R && X0 + TW + 2 * R <= W && Y0 >= 2 * R &&
-                          Y0 + TH + 2 * R <= band.h_img && Y0 + TH <= band.y_end;
-    // ---- pass 1: intermediate rows [Y0-R, Y0+TH+R), cols [X0-R, X0+TW+R)
-    if (tid < Ly::NT1) {
-        const int xi = tid % Ly::IW, s = tid / Ly::IW;
-        const int yi0 = s * Ly::SEG1;
-        const int nrows = min(Ly::SEG1, Ly::IH - yi0);
-        if (nrows > 0) {
-            const T* col = Us + yi0 * Ly::BW + xi + Ly::XOFF;
-            double* o = Is + yi0 * Ly::IP + xi;
-            const int gx = X0 - R + xi, gy0 = Y0 - R + yi0;
-            if (interior)
-                tb_walk<R, T, EXACT1, false, true, Ly::SEG1>(col, Ly::BW, nrows, gx, gy0, W, band,
-                                                             o, Ly::IP, rtab);
-            else
-                tb_walk<R, T, EXACT1, true, true, Ly::SEG1>(col, Ly::BW, nrows, gx, gy0, W, band,
-                                                            o, Ly::IP, rtab);
-        }
-    }
+    const bool interior = X0 >= Ly::HALO && X0 + Ly::TWK + Ly::HALO <= W && Y0 >= Ly::HALO &&
+                          Y0 + Ly::THK + Ly::HALO <= band.h_img && Y0 + Ly::THK <= band.y_end;
+    tbk_smem_pass<R, T, K, 1, EXACT1>(Us, IA, X0, Y0, W, band, interior, rtab);
     __syncthreads();
-    // ---- pass 2: output tile from the intermediate
-    if (tid < Ly::NT2) {
-        const int x = tid % TW, s = tid / TW;
+    if constexpr (K >= 3) {
+        tbk_smem_pass<R, T, K, 2, EXACT1>(IA, IB, X0, Y0, W, band, interior, rtab);
+        __syncthreads();
+    }
+    if constexpr (K >= 4) {
+        tbk_smem_pass<R, T, K, 3, EXACT1>(IB, IA, X0, Y0, W, band, interior, rtab);
+        __syncthreads();
+    }
+    // ---- pass K: the output tile from pass K-1
+    const double* last = (K % 2 == 0) ? IA : IB;  // pass K-1 wrote IA when K-1 is odd
+    constexpr int IWl = Ly::IW(K - 1);
+    constexpr int SEGK = Ly::THK / Ly::NSEG;
+    if (tid < Ly::TWK * Ly::NSEG) {
+        const int x = tid % Ly::TWK, s = tid / Ly::TWK;
         const int gx = X0 + x;
         if (interior || gx < W) {
-            const int y0 = s * Ly::SEG2;
-            const double* col = Is + y0 * Ly::IP + x;
+            const int y0 = s * SEGK;
+            const double* col = last + y0 * IWl + x;
             double* o = out + static_cast<size_t>(b) * out_plane +
                         static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
             if (interior)
-                tb_walk<R, double, false, false, false, Ly::SEG2>(col, Ly::IP, Ly::SEG2, gx,
-                                                                  Y0 + y0, W, band, o, out_pitch,
-                                                                  rtab);
+                tb_walk<R, double, false, false, false, SEGK>(col, IWl, SEGK, gx, Y0 + y0, W,
+                                                              band, o, out_pitch, rtab);
             else
-                tb_walk<R, double, false, true, false, Ly::SEG2>(col, Ly::IP, Ly::SEG2, gx,
-                                                                 Y0 + y0, W, band, o, out_pitch,
-                                                                 rtab);
+                tb_walk<R, double, false, true, false, SEGK>(col, IWl, SEGK, gx, Y0 + y0, W,
+                                                             band, o, out_pitch, rtab);
         }
+    }
+    if (band.push_rows) {  // row-band mode with the fused halo push
+        __syncthreads();
+        if (tid < Ly::TWK * Ly::NSEG) {
+            const int gx = X0 + tid % Ly::TWK, ya = Y0 + (tid / Ly::TWK) * SEGK;
+            if (gx < W) push_tail(band, out + static_cast<size_t>(b) * out_plane, out_pitch, gx, ya,
+                                  min(ya + SEGK, band.y_end));
+        }
+    }
+}
+
+template <int R, typename T, int K, bool EXACT1>
+cudaError_t launch_tmak(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                        size_t opl, cudaStream_t s) {
+    using Ly = TBKLay<R, T, K>;
+    if constexpr (Ly::SMEM > 227 * 1024) {
+        return cudaErrorNotSupported;
+    } else {
+        CUtensorMap map;
+        const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+        if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                            in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+            return cudaErrorNotSupported;
+        static std::atomic<unsigned long long> done{0};
+        if (cudaError_t e = ensure_smem(fast_tma_stepk<R, T, K, EXACT1>, Ly::SMEM, done)) return e;
+        dim3 grid((g.width + Ly::TWK - 1) / Ly::TWK, (g.height + Ly::THK - 1) / Ly::THK, g.batch);
+        note_kernel("fast_tma_stepk");
+        fast_tma_stepk<R, T, K, EXACT1><<<grid, Ly::NTT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                                        band_of(g));
+        return cudaGetLastError();
     }
 }
 
 template <int R, typename T, bool EXACT1>
-cudaError_t launch_tma2(const PlaneView& in, const Geometry& g, double* out, size_t op,
-                        size_t opl, cudaStream_t s) {
-    using Ly = TB2Lay<R, T>;
-    CUtensorMap map;
-    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
-    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
-                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
-        return cudaErrorNotSupported;
-    static std::atomic<unsigned long long> done{0};
-    if (cudaError_t e = ensure_smem(fast_tma_step2<R, T, EXACT1>, Ly::SMEM, done)) return e;
-    dim3 grid((g.width + TW - 1) / TW, (g.height + TH - 1) / TH, g.batch);
-    note_kernel("fast_tma_step2");
-    fast_tma_step2<R, T, EXACT1><<<grid, Ly::NTT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
-                                                                 band_of(g));
-    return cudaGetLastError();
+cudaError_t launch_tmak_passes(const PlaneView& in, const Geometry& g, int k, double* out,
+                               size_t op, size_t opl, cudaStream_t s) {
+    switch (k) {
+        case 2: return launch_tmak<R, T, 2, EXACT1>(in, g, out, op, opl, s);
+        case 3: return launch_tmak<R, T, 3, EXACT1>(in, g, out, op, opl, s);
+        case 4: return launch_tmak<R, T, 4, EXACT1>(in, g, out, op, opl, s);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 }  // namespace fastk
 
-// Two passes in one launch (radius <= kTb2Radius); cudaErrorNotSupported
-// when not applicable (caller falls back to two single passes).
+// k passes in one launch (2 <= k <= kTbMaxPasses, radius <= kTbRadius);
+// cudaErrorNotSupported when not applicable (caller runs fewer passes).
 template <int R>
-cudaError_t fast_launch_radius2(const PlaneView& in, const Geometry& g, double* out,
+cudaError_t fast_launch_radiusk(const PlaneView& in, const Geometry& g, int k, double* out,
                                 size_t out_pitch, size_t out_plane, cudaStream_t s) {
-    if constexpr (R <= fastk::kTb2Radius) {
+    if constexpr (R <= fastk::kTbRadius) {
         switch (in.dtype) {
             case OSBF_U8:
-                return fastk::launch_tma2<R, uint8_t, true>(in, g, out, out_pitch, out_plane, s);
+                return fastk::launch_tmak_passes<R, uint8_t, true>(in, g, k, out, out_pitch,
+                                                                   out_plane, s);
             case OSBF_F32:
-                return fastk::launch_tma2<R, float, false>(in, g, out, out_pitch, out_plane, s);
+                return fastk::launch_tmak_passes<R, float, false>(in, g, k, out, out_pitch,
+                                                                  out_plane, s);
             default:
-                return fastk::launch_tma2<R, double, false>(in, g, out, out_pitch, out_plane, s);
+                return fastk::launch_tmak_passes<R, double, false>(in, g, k, out, out_pitch,
+                                                                   out_plane, s);
         }
     }
     return cudaErrorNotSupported;

@@ -6,6 +6,6 @@ template cudaError_t fast_launch_radius<12>(const PlaneView&, const Geometry&, d
                                              size_t, double*, uint8_t*, cudaStream_t);
 }  // namespace osbf_gpu
 namespace osbf_gpu {
-template cudaError_t fast_launch_radius2<12>(const PlaneView&, const Geometry&, double*, size_t,
-                                              size_t, cudaStream_t);
+template cudaError_t fast_launch_radiusk<12>(const PlaneView&, const Geometry&, int, double*,
+                                              size_t, size_t, cudaStream_t);
 }  // namespace osbf_gpu

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(SLay<R, T>::NTS, SLay<R, T>::MINB)
                  warp * Ly::H_WARP;
 
     const int X0 = blockIdx.x * Ly::TWS;
-    const int Y0 = band.y_out0 + blockIdx.y * band_rows;
+    const int Y0 = band.y_out0 + tile_row(band) * band_rows;
     const int nout = min(band_rows, band.y_end - Y0);
     const int nchunks = (nout + 2 * R + CH - 1) / CH;
     const int b = blockIdx.z;

@@ -138,10 +138,10 @@ cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double
                       size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
                       cudaStream_t s, LaunchCounter& lc);
 
-// Two fast passes in one launch (temporal blocking).  Returns
-// cudaErrorNotSupported (nothing launched) when the radius / layout has no
-// two-pass kernel; the caller then runs two single passes.
-cudaError_t fast_step2(const PlaneView& in, const Geometry& g, int radius, double* out,
+// k = 2..4 fast passes in one launch (temporal blocking, radius <= 4).
+// Returns cudaErrorNotSupported (nothing launched) when the radius / layout /
+// k has no multi-pass kernel; the caller then runs fewer passes per launch.
+cudaError_t fast_stepk(const PlaneView& in, const Geometry& g, int radius, int k, double* out,
                        size_t out_pitch, size_t out_plane, cudaStream_t s, LaunchCounter& lc);
 
 // ---- utilities (osbf_capi.cu) ----------------------------------------------

@@ -19,6 +19,7 @@ ap.add_argument("--shape", default="256,1024,1024")
 ap.add_argument("--dtype", default="f64")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--tag", default="")
+ap.add_argument("--iters", type=int, default=1, help="passes per timed call (temporal blocking needs >= 2)")
 a = ap.parse_args()
 B, H, W = map(int, a.shape.split(","))
 ctx = ob.Context(0)
@@ -37,7 +38,7 @@ for r in map(int, a.radii.split(",")):
            "box": lambda: ctx.box_filter(x, r, 1, out=y),
            "osbf3d": lambda: ctx.osbf_3d(x, r, 1, out=y),
            "box3d": lambda: ctx.box_filter_3d(x, r, 1, out=y)}.get(
-               a.mode, lambda: ctx.iterate(x, r, 1, mode=a.mode, out=y))
+               a.mode, lambda: ctx.iterate(x, r, a.iters, mode=a.mode, out=y))
     for _ in range(3):
         run()
     kernel = ctx.last_kernel
@@ -54,9 +55,9 @@ for r in map(int, a.radii.split(",")):
         s.record(); run(); e.record()
         torch.cuda.synchronize(); ts.append(s.elapsed_time(e))
     c = clk.stop()
-    ts.sort(); ms = ts[len(ts) // 2]
+    ts.sort(); ms = ts[len(ts) // 2] / a.iters
     px = B * H * W
-    gbs = px * (in_b + 8) / (ms / 1e3) / 1e9
+    gbs = px * ((in_b + 8) + (a.iters - 1) * 16) / a.iters / (ms / 1e3) / 1e9
     print(json.dumps({"mode": a.mode, "tag": a.tag, "kernel": kernel, "r": r, "shape": [B, H, W],
                       "dtype": a.dtype, "ms_per_pass": round(ms, 4),
                       "gpx_per_s": round(px / ms / 1e6, 2), "alg_GBps": round(gbs, 1),
