@@ -179,6 +179,15 @@ int tb_env() {
     return k;
 }
 
+// OSBF_GPU_EXACT=table: every exact pass on the whole-table path (A/B runs).
+bool exact_table_forced() {
+    static const bool on = [] {
+        const char* v = std::getenv("OSBF_GPU_EXACT");
+        return v && std::strcmp(v, "table") == 0;
+    }();
+    return on;
+}
+
 // One pass in the requested mode: src (typed view) -> dst (fp64).
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
                      int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
@@ -187,7 +196,8 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
     // the exact GPU kernels (bit-identical to the reference, hence also
     // within the fast mode's tolerance), like the reference accepts any r.
     if (mode == OSBF_MODE_FAST && r > osbf_gpu::kFastMaxRadius) mode = OSBF_MODE_EXACT;
-    if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius) {
+    if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius &&
+        !exact_table_forced()) {
         // fused exact path: row carries + strip kernel (same bits as below)
         OSBF_CUDA(ctx->rowpfx.ensure(osbf_gpu::exact_fused_carry_elems(g) * sizeof(double)),
                   "alloc carries");
@@ -396,7 +406,7 @@ const char* osbf_gpu_last_error(void) { return g_last_error.c_str(); }
 const char* osbf_gpu_last_kernel(void) { return g_last_kernel; }
 
 osbf_status osbf_gpu_set_fast_kernel(const char* name) {
-    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "pair", "stream", "sep"};
+    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "stream", "sep"};
     if (!name || !name[0]) {
         osbf_gpu::g_fast_override.store(nullptr, std::memory_order_release);
         return OSBF_OK;

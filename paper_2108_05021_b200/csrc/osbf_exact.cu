@@ -105,6 +105,67 @@ __global__ void __launch_bounds__(256)
     const long long cols = static_cast<long long>(W) + 1;
     const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
     const double u = to_f64(in[b * in_plane + static_cast<size_t>(y) * in_pitch + x]);
+    const bool diag = means != nullptr || sel != nullptr;
+    if (!diag && x >= r && x + r < W && y >= r && y + r < H) {
+        // interior pixel: the 8 windows share a 4x4 grid of table corners,
+        // rows {y-r, y, y+1, y+r+1} x columns {x-r, x, x+1, x+r+1}; every sum
+        // keeps the reference's ((A-B)-C)+D (integral.hpp:48-49) and the
+        // division by the count is IEEE-exact (div_by_count)
+        const double* rp[4] = {C + static_cast<long long>(y - r) * cols,
+                               C + static_cast<long long>(y) * cols,
+                               C + static_cast<long long>(y + 1) * cols,
+                               C + static_cast<long long>(y + r + 1) * cols};
+        const int co[4] = {x - r, x, x + 1, x + r + 1};
+        double g[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) g[a][c] = __ldg(rp[a] + co[c]);
+        // (ca, cb, ra, rb) per window in reference order (core.hpp:212-225)
+        constexpr int W8[8][4] = {{0, 2, 1, 3}, {1, 3, 1, 3}, {1, 3, 0, 2}, {0, 2, 0, 2},
+                                  {0, 2, 0, 3}, {1, 3, 0, 3}, {0, 3, 1, 3}, {0, 3, 0, 2}};
+        const double nq = static_cast<double>((r + 1) * (r + 1));
+        const double nh = static_cast<double>((r + 1) * (2 * r + 1));
+        const double yq = __ddiv_rn(1.0, nq), yh = __ddiv_rn(1.0, nh);
+        double av[8], dv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int ca = W8[i][0], cb = W8[i][1], ra = W8[i][2], rb = W8[i][3];
+            const double sm =
+                __dadd_rn(__dsub_rn(__dsub_rn(g[rb][cb], g[rb][ca]), g[ra][cb]), g[ra][ca]);
+            av[i] = div_by_count(sm, i < 4 ? nq : nh, i < 4 ? yq : yh);
+            dv[i] = fabs(__dsub_rn(av[i], u));
+        }
+        double best = 0.0;
+        const double dsum = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
+        if (fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL)) {
+            // all |a_i - u| finite: a stable depth-3 tournament returns the
+            // first minimum, the reference's strict < (filters2d.hpp:78)
+            auto pick = [](double& d0, double& a0, double d1, double a1) {
+                const bool t = d1 < d0;
+                d0 = t ? d1 : d0;
+                a0 = t ? a1 : a0;
+            };
+            pick(dv[0], av[0], dv[1], av[1]);
+            pick(dv[2], av[2], dv[3], av[3]);
+            pick(dv[4], av[4], dv[5], av[5]);
+            pick(dv[6], av[6], dv[7], av[7]);
+            pick(dv[0], av[0], dv[2], av[2]);
+            pick(dv[4], av[4], dv[6], av[6]);
+            pick(dv[0], av[0], dv[4], av[4]);
+            best = av[0];
+        } else {  // non-finite samples: the sequential rule never selects them
+            double best_abs = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (dv[i] < best_abs) {
+                    best_abs = dv[i];
+                    best = av[i];
+                }
+        }
+        out[b * out_plane + static_cast<size_t>(y) * out_pitch + x] = best;
+        return;
+    }
     double best = 0.0;
     double best_abs = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     int best_id = 0;

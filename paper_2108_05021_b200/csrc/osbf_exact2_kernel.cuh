@@ -63,6 +63,10 @@ __device__ __forceinline__ bool table_value_safe(double v) {
 
 namespace ex2 {
 
+#ifndef EXACT_BR32_MAX
+#define EXACT_BR32_MAX 6  // largest radius walking 32-row blocks (measured: r = 7, 8 faster at 16)
+#endif
+
 constexpr int TW = 32;   // output columns per strip
 constexpr int SW = 16;   // spacing of the stored row carries (columns)
 constexpr int BR = 32;   // rows per block (radii <= 8; larger radii use 16, see XLay)
@@ -75,7 +79,7 @@ struct XLay {
     // rows per block: 16 above r=8 halves the U / row-sum / ring footprint
     // (r=16: 149 KB -> 74 KB, one CTA per SM -> three); the single-phase
     // schedule (SP) always uses 16
-    static constexpr int BR = (SP || R > 8) ? 16 : ex2::BR;
+    static constexpr int BR = (SP || R > EXACT_BR32_MAX) ? 16 : ex2::BR;
     // staged U columns: [xs, xs + NU) with xs = floor((X0-R)/SW)*SW >= X0-R-SW+1,
     // covering up to X0 + TW + R - 1
     static constexpr int NU = TW + 2 * R + SW;

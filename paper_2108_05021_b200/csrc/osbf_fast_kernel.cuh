@@ -226,7 +226,8 @@ struct ColFactors {
 
 // Means, |a-u| selection and the store for one pixel (S = the eight window
 // sums in reference order, u = the centre sample).
-template <int R, bool EXACT_DIV, bool BORDER, bool DIAG, bool FAST_SEQ = false>
+template <int R, bool EXACT_DIV, bool BORDER, bool DIAG, bool FAST_SEQ = false,
+          bool INT_SEL = false>
 __device__ __forceinline__ double select_store(const double (&S)[8], double u, int gx, int gy,
                                              int W, int H, int b, double* __restrict__ o,
                                              double* __restrict__ means,
@@ -290,7 +291,31 @@ __device__ __forceinline__ double select_store(const double (&S)[8], double u, i
     // register-capped kernels); else a stable depth-3 tournament.  Finite
     // input assumed (non-finite samples: use exact mode).
     double best;
-    if constexpr (FAST_SEQ) {
+    if constexpr (INT_SEL) {
+        // |d| compared on the integer pipe: for finite doubles the sign-cleared
+        // bit patterns order like the magnitudes (ties equal), so a stable
+        // tournament on (key, d) picks the same first minimum
+        double d[8];
+        long long k[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            d[i] = fma(S[i], rc[i], -u);
+            k[i] = __double_as_longlong(d[i]) & 0x7fffffffffffffffLL;
+        }
+        auto pk = [](long long& ka, double& da, long long kc, double dc) {
+            const bool p = kc < ka;
+            ka = p ? kc : ka;
+            da = p ? dc : da;
+        };
+        pk(k[0], d[0], k[1], d[1]);
+        pk(k[2], d[2], k[3], d[3]);
+        pk(k[4], d[4], k[5], d[5]);
+        pk(k[6], d[6], k[7], d[7]);
+        pk(k[0], d[0], k[2], d[2]);
+        pk(k[4], d[4], k[6], d[6]);
+        pk(k[0], d[0], k[4], d[4]);
+        best = d[0];
+    } else if constexpr (FAST_SEQ) {
         best = fma(S[0], rc[0], -u);
 #pragma unroll
         for (int i = 1; i < 8; ++i) {
@@ -502,7 +527,8 @@ struct TLay {
     static constexpr size_t SMEM = TILE_BYTES + 128;  // + alignment slack
 };
 
-template <int R, typename T, bool EXACT_DIV, bool BORDER, class Ly = TLay<R, T>, bool SEQ = false>
+template <int R, typename T, bool EXACT_DIV, bool BORDER, class Ly = TLay<R, T>, bool SEQ = false,
+          bool ISEL = false>
 __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, int Y0, int W,
                                             const Band& band, int b, double* __restrict__ outp,
                                             size_t out_pitch, const double* __restrict__ rtab) {
@@ -546,8 +572,8 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
                                  P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
                                  P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
                                  Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
-            select_store<R, EXACT_DIV, BORDER, false, SEQ>(S, Uc[y + R], gx, gy, W, H, b, o,
-                                                           nullptr, nullptr, cf, rtab);
+            select_store<R, EXACT_DIV, BORDER, false, SEQ, ISEL>(S, Uc[y + R], gx, gy, W, H, b,
+                                                                 o, nullptr, nullptr, cf, rtab);
             o += out_pitch;
         }
     }
@@ -559,6 +585,7 @@ __device__ __forceinline__ void direct_walk(const T* __restrict__ Us, int X0, in
 template <int R, typename T, int VAR>
 struct TVar {
     static constexpr bool SEQ = VAR == 1;
+    static constexpr bool ISEL = VAR == 2;
     using Ly = TLay<R, T, VAR == 1 ? 64 : 0>;
     static constexpr int MINB = VAR == 1 ? (R <= 2 ? 4 : 3) : (R <= 2 ? 3 : (R <= 4 ? 2 : 1));
 };
@@ -569,6 +596,7 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : TVar<R, T, 
                   size_t out_pitch, size_t out_plane, int W, Band band) {
     using Ly = typename TVar<R, T, VAR>::Ly;
     constexpr bool SEQ = TVar<R, T, VAR>::SEQ;
+    constexpr bool ISEL = TVar<R, T, VAR>::ISEL;
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t bar;
     __shared__ double rtab[Ly::NRT];
@@ -586,9 +614,11 @@ __global__ void __launch_bounds__(NT, EXACT_DIV ? (R <= 2 ? 2 : 1) : TVar<R, T, 
     double* outp = out + static_cast<size_t>(b) * out_plane;
     if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
         Y0 + Ly::THT <= band.y_end)
-        direct_walk<R, T, EXACT_DIV, false, Ly, SEQ>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
+        direct_walk<R, T, EXACT_DIV, false, Ly, SEQ, ISEL>(Us, X0, Y0, W, band, b, outp, out_pitch,
+                                                           rtab);
     else
-        direct_walk<R, T, EXACT_DIV, true, Ly, SEQ>(Us, X0, Y0, W, band, b, outp, out_pitch, rtab);
+        direct_walk<R, T, EXACT_DIV, true, Ly, SEQ, ISEL>(Us, X0, Y0, W, band, b, outp, out_pitch,
+                                                          rtab);
     if (band.push_rows) {  // row-band mode with the fused halo push
         const int gx = X0 + threadIdx.x % TW, ya = Y0 + (threadIdx.x / TW) * Ly::SEGT;
         if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
@@ -615,7 +645,7 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
     static std::atomic<unsigned long long> done{0};
     if (cudaError_t e = ensure_smem(fast_tma_step<R, T, EXACT_DIV, VAR>, Ly::SMEM, done)) return e;
     dim3 grid((g.width + TW - 1) / TW, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
-    note_kernel(VAR ? "fast_tma_step (seq)" : "fast_tma_step");
+    note_kernel(VAR == 1 ? "fast_tma_step (seq)" : (VAR == 2 ? "fast_tma_step (intsel)" : "fast_tma_step"));
     fast_tma_step<R, T, EXACT_DIV, VAR><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
                                                                    band_of(g));
     return cudaGetLastError();
@@ -1022,6 +1052,17 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
                 case OSBF_U8: e = launch_pair<R, uint8_t, true>(in, g, out, op, opl, s); break;
                 case OSBF_F32: e = launch_pair<R, float, false>(in, g, out, op, opl, s); break;
                 default: e = launch_pair<R, double, false>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R <= kTmaRadius && !DIAG) {
+        if (fast_allowed("tmaint", false)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_tma<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_tma<R, float, false, 2>(in, g, out, op, opl, s); break;
+                default: e = launch_tma<R, double, false, 2>(in, g, out, op, opl, s); break;
             }
             if (e != cudaErrorNotSupported) return e;
         }
