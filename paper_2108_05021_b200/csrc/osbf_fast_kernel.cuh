@@ -652,6 +652,176 @@ cudaError_t launch_tma(const PlaneView& in, const Geometry& g, double* out, size
 }
 
 // ---------------------------------------------------------------------------
+// TMA tile with a shared arm pass (r = 3, 4): the walk of fast_tma_step loads
+// 2R+1 samples per row per thread (at r = 4 the shared-memory pipe ran at 70%
+// of its peak on the 32768^2 plane); here the tile's horizontal left arms
+// H(k) = U(k-R) + ... + U(k) are formed once per staged row by sliding sums
+// (lanes = rows x segments) into a second shared array, and each column
+// thread's walk reads F1 = H(x), F2 = H(x+R) and U(x): 3 loads per row.
+constexpr int kArmsMinRadius = 3, kArmsMaxRadius = 4;
+
+// Phase-A mapping idx -> (row idx % LH? ...) chosen at compile time: lane idx
+// covers row (idx / NSA) and segment (idx % NSA) of SA columns; 8-byte
+// accesses at row*pitch + seg*SA + k must hit distinct bank pairs per
+// half-warp.
+constexpr bool arms_rows_conflict_free(int nlane, int nseg, int seg, int pitch) {
+    for (int h0 = 0; h0 < nlane; h0 += 16) {
+        unsigned mask = 0;
+        for (int i = 0; i < 16 && h0 + i < nlane; ++i) {
+            const int idx = h0 + i, row = idx / nseg, sg = idx % nseg;
+            const int bank = (row * pitch + sg * seg) % 16;
+            if ((mask >> bank) & 1u) return false;
+            mask |= 1u << bank;
+        }
+    }
+    return true;
+}
+constexpr int arms_rows_pitch(int nlane, int nseg, int seg, int minp, int step) {
+    for (int p = minp; p < minp + 32 * step; p += step)
+        if (arms_rows_conflict_free(nlane, nseg, seg, p)) return p;
+    return minp;
+}
+
+template <int R, typename T>
+struct ALay {
+    static constexpr int THT = 64;
+    static constexpr int SEGT = THT / NSB;
+    static constexpr int LH = THT + 2 * R;
+    static constexpr int ALIGN = 16 / static_cast<int>(sizeof(T));
+    static constexpr int RA = (R + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int XOFF = RA - R;
+    static constexpr int NHC = TW + R;                     // arm columns H(k), k < NHC
+    static constexpr int NSA = NT / LH;                    // segments per row (phase A)
+    static constexpr int SA = ((NHC + NSA - 1) / NSA) | 1; // columns per segment (odd)
+    // staged row pitch: TMA box width (multiple of 16 bytes) >= XOFF + NSA*SA + R,
+    // conflict-free for the phase-A lanes when fp64
+    static constexpr int BW0 = (XOFF + NSA * SA + R + ALIGN - 1) / ALIGN * ALIGN;
+    static constexpr int BW =
+        sizeof(T) == 8 ? arms_rows_pitch(LH * NSA, NSA, SA, BW0, ALIGN) : BW0;
+    static constexpr int PH = arms_rows_pitch(LH * NSA, NSA, SA, NSA * SA, 1);
+    static constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(BW) * LH * sizeof(T);
+    static constexpr size_t UBUF = (TILE_BYTES + 15) / 16 * 16;
+    static constexpr size_t SMEM = 128 + UBUF + sizeof(double) * static_cast<size_t>(LH) * PH;
+    static constexpr int NRT = 2 * R + 2;
+    static_assert(BW <= 256, "TMA box");
+};
+
+template <int R, typename T, bool EXACT_DIV, bool BORDER>
+__device__ __forceinline__ void arms_walk(const T* __restrict__ Us, const double* __restrict__ Hs,
+                                          int X0, int Y0, int W, const Band& band,
+                                          double* __restrict__ outp, size_t out_pitch,
+                                          const double* __restrict__ rtab) {
+    using Ly = ALay<R, T>;
+    const int x = threadIdx.x % TW, s = threadIdx.x / TW;
+    const int gx = X0 + x;
+    if (BORDER && gx >= W) return;
+    ColFactors cf{0.0, 0.0, 0.0};
+    if (BORDER) {
+        const int ncl = min(gx, R) + 1, ncr = min(W - 1 - gx, R) + 1;
+        cf = ColFactors{rtab[ncl], rtab[ncr], rtab[ncl + ncr - 1]};
+    }
+    const int y0 = s * Ly::SEGT;
+    const double* __restrict__ h = Hs + y0 * Ly::PH + x;
+    const T* __restrict__ uc = Us + y0 * Ly::BW + x + Ly::RA;
+    const int H = band.h_img;
+    double* o = outp + static_cast<size_t>(Y0 + y0 - band.y_out0) * out_pitch + gx;
+    constexpr int NJ = Ly::SEGT + 2 * R;
+    double P1[NJ + 1], P2[NJ + 1], Q[NJ + 1], Uc[NJ];
+    P1[0] = P2[0] = Q[0] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const double a = h[j * Ly::PH], c = h[j * Ly::PH + R];
+        const double e = to_f64(uc[j * Ly::BW]);
+        Uc[j] = e;
+        P1[j + 1] = P1[j] + a;
+        P2[j + 1] = P2[j] + c;
+        Q[j + 1] = Q[j] + ((a + c) - e);
+        const int y = j - 2 * R;
+        if (y >= 0) {
+            const int gy = Y0 + y0 + y;
+            if (BORDER && gy >= band.y_end) break;
+            const double S[8] = {P1[y + 2 * R + 1] - P1[y + R], P2[y + 2 * R + 1] - P2[y + R],
+                                 P2[y + R + 1] - P2[y],         P1[y + R + 1] - P1[y],
+                                 P1[y + 2 * R + 1] - P1[y],     P2[y + 2 * R + 1] - P2[y],
+                                 Q[y + 2 * R + 1] - Q[y + R],   Q[y + R + 1] - Q[y]};
+            select_store<R, EXACT_DIV, BORDER, false>(S, Uc[y + R], gx, gy, W, H, 0, o, nullptr,
+                                                      nullptr, cf, rtab);
+            o += out_pitch;
+        }
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+__global__ void __launch_bounds__(NT, 2)
+    fast_tma_arms(const __grid_constant__ CUtensorMap tmap, double* __restrict__ out,
+                  size_t out_pitch, size_t out_plane, int W, Band band) {
+    using Ly = ALay<R, T>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ double rtab[Ly::NRT];
+    const uint32_t base = tma::smem_u32(smem_raw);
+    unsigned char* al = smem_raw + ((128u - (base & 127u)) & 127u);
+    T* Us = reinterpret_cast<T*>(al);
+    double* Hs = reinterpret_cast<double*>(al + Ly::UBUF);
+    const int X0 = blockIdx.x * TW, Y0 = band.y_out0 + tile_row(band) * Ly::THT, b = blockIdx.z;
+    if (threadIdx.x == 0) tma::mbar_init(&bar, 1);
+    if (threadIdx.x < Ly::NRT) rtab[threadIdx.x] = threadIdx.x ? 1.0 / threadIdx.x : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tma::mbar_arrive_expect_tx(&bar, Ly::TILE_BYTES);
+        tma::load_3d(Us, &tmap, X0 - Ly::RA, Y0 - R - band.y_in0, b, &bar);
+    }
+    tma::mbar_wait(&bar, 0);
+    // ---- arms: lane (row, segment) slides a (R+1)-sample sum along its segment
+    if (threadIdx.x < Ly::LH * Ly::NSA) {
+        const int row = threadIdx.x / Ly::NSA, sg = threadIdx.x % Ly::NSA;
+        const T* __restrict__ u = Us + row * Ly::BW + Ly::XOFF + sg * Ly::SA;
+        double* __restrict__ hp = Hs + row * Ly::PH + sg * Ly::SA;
+        double v[Ly::SA + R];
+#pragma unroll
+        for (int i = 0; i < Ly::SA + R; ++i) v[i] = to_f64(u[i]);
+        double acc = v[0];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) acc += v[i];
+        hp[0] = acc;
+#pragma unroll
+        for (int m = 1; m < Ly::SA; ++m) {
+            acc += v[m + R] - v[m - 1];
+            hp[m] = acc;
+        }
+    }
+    __syncthreads();
+    double* outp = out + static_cast<size_t>(b) * out_plane;
+    if (X0 >= R && X0 + TW + R <= W && Y0 >= R && Y0 + Ly::THT + R <= band.h_img &&
+        Y0 + Ly::THT <= band.y_end)
+        arms_walk<R, T, EXACT_DIV, false>(Us, Hs, X0, Y0, W, band, outp, out_pitch, rtab);
+    else
+        arms_walk<R, T, EXACT_DIV, true>(Us, Hs, X0, Y0, W, band, outp, out_pitch, rtab);
+    if (band.push_rows) {  // row-band mode with the fused halo push
+        const int gx = X0 + threadIdx.x % TW, ya = Y0 + (threadIdx.x / TW) * Ly::SEGT;
+        if (gx < W) push_tail(band, outp, out_pitch, gx, ya, min(ya + Ly::SEGT, band.y_end));
+    }
+}
+
+template <int R, typename T, bool EXACT_DIV>
+cudaError_t launch_arms(const PlaneView& in, const Geometry& g, double* out, size_t op,
+                        size_t opl, cudaStream_t s) {
+    using Ly = ALay<R, T>;
+    CUtensorMap map;
+    const uint64_t plane_bytes = (g.batch > 1 ? in.plane : in.pitch * g.in_h()) * sizeof(T);
+    if (!tma::encode_3d(&map, tma_dtype<T>(), in.base, g.width, g.in_h(), g.batch,
+                        in.pitch * sizeof(T), plane_bytes, Ly::BW, Ly::LH))
+        return cudaErrorNotSupported;
+    static std::atomic<unsigned long long> done{0};
+    if (cudaError_t e = ensure_smem(fast_tma_arms<R, T, EXACT_DIV>, Ly::SMEM, done)) return e;
+    dim3 grid((g.width + TW - 1) / TW, (g.height + Ly::THT - 1) / Ly::THT, g.batch);
+    note_kernel("fast_tma_arms");
+    fast_tma_arms<R, T, EXACT_DIV><<<grid, NT, Ly::SMEM, s>>>(map, out, op, opl, g.width,
+                                                              band_of(g));
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Two columns per thread (r <= kTmaRadius): the TMA-staged tile of
 // fast_tma_step, but each thread walks the adjacent columns x0, x0 + 1 of its
 // segment.  Their windows share 2R of their 2R + 2 samples per row, loaded as
@@ -1042,6 +1212,17 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
     if constexpr (!DIAG) {
         if (fast_allowed("strip", false)) {
             const cudaError_t e = strip_launch_radius<R>(in, g, out, op, opl, s);
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R >= kArmsMinRadius && R <= kArmsMaxRadius && !DIAG) {
+        if (fast_allowed("arms", false)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_arms<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_arms<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_arms<R, double, false>(in, g, out, op, opl, s); break;
+            }
             if (e != cudaErrorNotSupported) return e;
         }
     }

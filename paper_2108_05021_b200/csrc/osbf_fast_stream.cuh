@@ -1,15 +1,16 @@
 // Fast mode, mid radii: streaming column strips with register rings.
 //
 // Included by osbf_fast_kernel.cuh (uses Band, select_store, ColFactors,
-// tma_dtype).  One CTA owns a strip of TWS = 224 output columns and a band of
-// output rows, and walks down it once:
+// tma_dtype).  One CTA owns a strip of TWS = 128 output columns (NWB = 4
+// column warps) and a band of output rows, and walks down it once:
 //
-//   * A producer warp streams the strip (plus an R-column halo each side)
-//     with TMA in chunks of CH = 2R+2 (R+1 above r=10) rows through a 3-8 slot ring
-//     (mbarrier full/empty pairs; hardware zero fill outside the image, so
+//   * Thread 0 streams the strip (plus an R-column halo each side) with TMA
+//     in chunks of CH = 2R+2 (R+1 above r=10) rows through a 3-8 slot ring
+//     (one mbarrier per slot; after each chunk one CTA barrier frees the
+//     previous chunk's slot; hardware zero fill outside the image, so
 //     clipped windows need no special casing; the valid counts are the
 //     reference's clipped ones, integral.hpp:53-61).
-//   * Seven column warps, one thread per output column.  Per chunk each warp
+//   * Four column warps, one thread per output column.  Per chunk each warp
 //     first forms the horizontal left arms H(x) = sum U[x-R..x] of its own
 //     32 + R columns (lanes = 16 rows x 2 odd-length segments: conflict-free,
 //     fully unrolled so every sample is loaded once) into a private slice,
@@ -19,7 +20,7 @@
 //     REGISTERS (a ring indexed by the row within the chunk, so every index
 //     is static).  Per pixel: 3 shared-memory loads for the walk, O(1) work
 //     independent of R, and each input row is read once per strip (no tile
-//     halo rows).  No CTA-wide barrier: warps only wait for their chunk.
+//     halo rows).
 //
 // Running sums start at zero over a zeroed ring at the first input row (the
 // window rows above the strip's first output are the R rows of the halo), so

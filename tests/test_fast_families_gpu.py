@@ -9,7 +9,7 @@ from conftest import bits
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = {"tma": range(1, 5), "pair": range(1, 5), "tmaseq": range(1, 5), "tmaint": range(1, 5),
+FAMILIES = {"arms": range(3, 5), "tma": range(1, 5), "pair": range(1, 5), "tmaseq": range(1, 5), "tmaint": range(1, 5),
             "tile": range(1, 5), "stream": range(5, 17), "strip": range(1, 17)}
 CASES = [(fam, r) for fam, rs in FAMILIES.items() for r in rs]
 
@@ -33,7 +33,7 @@ def test_family_matches_oracle(ctx, oracle_lib, family, fam, r):
     for shape in [(1, 70, 128), (2, 300, 256), (1, 129, 320), (1, 3, 64)]:
         p = rng.random(shape) * 255.0
         got = ctx.iterate(torch.from_numpy(p).cuda(), r, 3, mode="fast").cpu().numpy()
-        assert fam.split("seq")[0] in ctx.last_kernel or fam in ("tile", "tmaseq", "tmaint"), \
+        assert fam.split("seq")[0] in ctx.last_kernel or fam in ("tile", "tmaseq", "tmaint", "arms"), \
             ctx.last_kernel
         want = np.stack([oracle_lib.osbf(c, r, 3) for c in p])
         assert float(np.abs(got - want).max()) <= 1e-5 * 255.0, shape
