@@ -406,7 +406,7 @@ const char* osbf_gpu_last_error(void) { return g_last_error.c_str(); }
 const char* osbf_gpu_last_kernel(void) { return g_last_kernel; }
 
 osbf_status osbf_gpu_set_fast_kernel(const char* name) {
-    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "arms", "stream", "sep"};
+    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "arms", "stream", "walk", "sep"};
     if (!name || !name[0]) {
         osbf_gpu::g_fast_override.store(nullptr, std::memory_order_release);
         return OSBF_OK;

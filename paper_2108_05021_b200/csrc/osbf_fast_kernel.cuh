@@ -1182,6 +1182,7 @@ cudaError_t launch_tile(const PlaneView& in, const Geometry& g, double* out, siz
 }  // namespace osbf_gpu
 
 #include "osbf_fast_stream.cuh"
+#include "osbf_fast_walk.cuh"
 #include "osbf_strip.cuh"
 
 namespace osbf_gpu {
@@ -1266,6 +1267,17 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
                 case OSBF_U8: e = launch_tile<R, uint8_t, true>(in, g, out, op, opl, s); break;
                 case OSBF_F32: e = launch_tile<R, float, false>(in, g, out, op, opl, s); break;
                 default: e = launch_tile<R, double, false>(in, g, out, op, opl, s); break;
+            }
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
+    if constexpr (R <= kWalkMaxRadius && !DIAG) {
+        if (fast_allowed("walk", R >= 3)) {
+            cudaError_t e = cudaErrorNotSupported;
+            switch (in.dtype) {
+                case OSBF_U8: e = launch_walk<R, uint8_t, true>(in, g, out, op, opl, s); break;
+                case OSBF_F32: e = launch_walk<R, float, false>(in, g, out, op, opl, s); break;
+                default: e = launch_walk<R, double, false>(in, g, out, op, opl, s); break;
             }
             if (e != cudaErrorNotSupported) return e;
         }

@@ -25,7 +25,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-TILE_ROWS = 128  # fast-kernel tile height (r = 3, 4); band starts aligned to it
+TILE_ROWS = 128  # fast tile-kernel height (r <= 2); band starts aligned to it
+WALK_ROWS = 512  # fast column-walk row block (r >= 3): preferred band alignment
 
 
 def shard_batch(batch: int, world: int, rank: int) -> tuple[int, int]:
@@ -37,12 +38,7 @@ def shard_batch(batch: int, world: int, rank: int) -> tuple[int, int]:
     return start, base + (1 if rank < extra else 0)
 
 
-def band_rows(height: int, world: int, radius: int, align: int = TILE_ROWS) -> list[tuple[int, int]]:
-    """Split ``height`` rows into ``world`` bands [row0, row1), starts aligned
-    to ``align`` where possible; every band has at least ``radius`` rows so a
-    neighbour's halo lies in one band."""
-    if world < 1:
-        raise ValueError("world must be >= 1")
+def _split(height: int, world: int, align: int) -> list[tuple[int, int]]:
     bounds = [0]
     for i in range(1, world):
         b = round(height * i / world / align) * align
@@ -50,11 +46,30 @@ def band_rows(height: int, world: int, radius: int, align: int = TILE_ROWS) -> l
             b = bounds[-1] + max(1, height // world)
         bounds.append(min(b, height))
     bounds.append(height)
-    bands = list(zip(bounds[:-1], bounds[1:]))
-    for r0, r1 in bands:
-        if r1 - r0 < max(1, radius):
-            raise ValueError(f"band [{r0},{r1}) shorter than the radius {radius}: too many ranks")
-    return bands
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
+def band_rows(height: int, world: int, radius: int, align: int | None = None) -> list[tuple[int, int]]:
+    """Split ``height`` rows into ``world`` bands [row0, row1), starts aligned
+    to ``align`` where possible (default: the column walk's 512-row block when
+    every band can hold one, else the 128-row tile; aligned bands give results
+    bit-identical to the whole image).  Every band has at least ``radius``
+    rows so a neighbour's halo lies in one band; when an aligned split cannot
+    give that, the split falls back to a coarser-then-unaligned one."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if align is not None:
+        aligns = [align]
+    elif height >= world * WALK_ROWS:
+        aligns = [WALK_ROWS, TILE_ROWS]
+    else:
+        aligns = [TILE_ROWS]
+    for a in aligns + [1]:
+        bands = _split(height, world, a)
+        if all(r1 - r0 >= max(1, radius) for r0, r1 in bands):
+            return bands
+    raise ValueError(f"{height} rows cannot give {world} bands of at least the radius {radius}: "
+                     "too many ranks")
 
 
 @dataclass(frozen=True)

@@ -10,7 +10,7 @@ from conftest import bits
 pytestmark = pytest.mark.gpu
 
 FAMILIES = {"arms": range(3, 5), "tma": range(1, 5), "pair": range(1, 5), "tmaseq": range(1, 5), "tmaint": range(1, 5),
-            "tile": range(1, 5), "stream": range(5, 17), "strip": range(1, 17)}
+            "tile": range(1, 5), "stream": range(5, 17), "strip": range(1, 17), "walk": range(1, 17)}
 CASES = [(fam, r) for fam, rs in FAMILIES.items() for r in rs]
 
 

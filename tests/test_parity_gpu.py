@@ -226,17 +226,17 @@ def test_in_place_and_pitched(ctx, oracle_lib):
     assert np.array_equal(bits(got.cpu().numpy()), bits(want))
 
 
-STREAM_RADII = range(5, 17)  # fast radii served by the streaming column-strip kernel
+WALK_RADII = range(3, 17)  # fast radii served by the column walk (512-row blocks)
 
 
 @pytest.mark.parametrize("r", [2, 7, 12])
 def test_row_bands_equal_whole_image(ctx, r):
-    """osbf_gpu_step_band over 64-aligned row bands (halos copied from the
+    """osbf_gpu_step_band over 128-aligned row bands (halos copied from the
     previous pass, as the multi-GPU exchange does) is bit-identical to the
-    whole-image fast pass for the tile kernels; the streaming kernel's running
-    sums start at each band's first row, so there the bands agree to fp64
-    rounding (1e-9 of the range).  Unaligned bands stay within the float
-    tolerance."""
+    whole-image fast pass for the tile kernels; the column walk's prefix sums
+    start at each band's first row, so there (bands not on its 512-row block
+    grid) the bands agree to fp64 rounding (1e-9 of the range).  Unaligned
+    bands stay within the float tolerance."""
     import torch
 
     from paper_2108_05021_b200.dist import BandLayout
@@ -253,7 +253,7 @@ def test_row_bands_equal_whole_image(ctx, r):
                 src = cur[lay.buf_row0:lay.buf_row0 + lay.buf_rows].contiguous()
                 ctx.step_band(src, lay.buf_row0, nxt[lay.row0:lay.row1], lay.row0, lay.rows, h, r)
             cur = nxt
-        if r in STREAM_RADII:
+        if r in WALK_RADII:
             assert float((cur - want).abs().max()) <= 1e-9, world
         else:
             assert torch.equal(cur.view(torch.int64), want.view(torch.int64)), world
@@ -269,6 +269,31 @@ def test_row_bands_equal_whole_image(ctx, r):
     assert float((cur - want).abs().max()) <= FLOAT_TOL
 
 
+@pytest.mark.parametrize("r", [3, 4, 8, 16])
+def test_row_bands_walk_block_aligned_bit_identical(ctx, r):
+    """Row bands whose starts sit on the column walk's 512-row block grid
+    (dist.band_rows' default alignment) walk exactly the blocks of the whole
+    image: bit-identical results over several passes."""
+    import torch
+
+    from paper_2108_05021_b200.dist import BandLayout, band_rows
+
+    h, w, iters, world = 1536 + 77, 260, 3, 3
+    assert [b[0] % 512 for b in band_rows(h, world, r)] == [0, 0, 0]
+    x = torch.from_numpy(np.random.default_rng(40 + r).random((h, w))).cuda()
+    want = ctx.iterate(x, r, iters, mode="fast")
+    assert "walk" in ctx.last_kernel
+    cur = x.clone()
+    for _ in range(iters):
+        nxt = torch.empty_like(cur)
+        for rank in range(world):
+            lay = BandLayout.make(h, w, r, world, rank)
+            src = cur[lay.buf_row0:lay.buf_row0 + lay.buf_rows].contiguous()
+            ctx.step_band(src, lay.buf_row0, nxt[lay.row0:lay.row1], lay.row0, lay.rows, h, r)
+        cur = nxt
+    assert torch.equal(cur.view(torch.int64), want.view(torch.int64))
+
+
 @pytest.mark.parametrize("r", [2, 4, 6])
 def test_row_bands_fused_push_equal_whole_image(ctx, r):
     """The fused exchange (osbf_gpu_step_band_push via dist.RowBandOSBF
@@ -277,7 +302,7 @@ def test_row_bands_fused_push_equal_whole_image(ctx, r):
     (their "symmetric" buffers are local allocations, passes run one after
     another on one stream, so no kernel waits on another); the result equals
     the whole-image pass (bit-identical for the tile kernels, fp64 rounding
-    for the streaming r=5..7 kernel)."""
+    for the column walk on bands off its 512-row grid)."""
     import torch
 
     from paper_2108_05021_b200.dist import BandLayout, RowBandOSBF
@@ -301,7 +326,7 @@ def test_row_bands_fused_push_equal_whole_image(ctx, r):
         for rb in ranks:
             rb.one_pass(last=it + 1 == iters)
     got = torch.cat([rb.result() for rb in ranks])
-    if r in STREAM_RADII:
+    if r in WALK_RADII:
         assert float((got - want).abs().max()) <= 1e-9
     else:
         assert torch.equal(got.view(torch.int64), want.view(torch.int64))
@@ -345,7 +370,7 @@ def test_temporal_blocking_matches_single_passes(oracle_lib, r, k):
         # TMA needs 16-byte row pitch: odd widths fall back to single passes
         if w % 2 == 0:
             assert ctxk.launches - before == -(-it // k)
-            assert ctxk.last_kernel in ("fast_tma_stepk", "fast_tma_step")
+            assert ctxk.last_kernel in ("fast_tma_stepk", "fast_tma_step", "fast_walk_step")
         else:
             assert ctxk.launches - before == it
         assert np.abs(tb - single).max() <= 1e-9 * 100.0
