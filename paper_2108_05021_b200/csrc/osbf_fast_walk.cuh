@@ -250,16 +250,26 @@ cudaError_t launch_walk(const PlaneView& in, const Geometry& g, double* out, siz
         return cudaErrorNotSupported;
     static std::atomic<unsigned long long> done{0};
     if (cudaError_t e = ensure_smem(fast_walk_step<R, T, EXACT_DIV>, Ly::SMEM, done)) return e;
-    // 512-row blocks (each re-reads a 2R-row halo): a single plane still fills
-    // the SMs.  Block boundaries sit at fixed global rows, never depending on
-    // the batch or on a row-band split aligned to them.
+    // Row blocks (each re-reads a 2R-row halo) sit at fixed global rows,
+    // never depending on the batch or on a row-band split aligned to them.
     const int strips = (g.width + Ly::SW - 1) / Ly::SW;
     static const int kBand = [] {
         const char* e = getenv("OSBF_GPU_WALK_BAND");  // diagnostic override
         const int v = e ? atoi(e) : 0;
-        return v >= 64 ? v : 512;
+        return v >= 64 ? v : 0;
     }();
-    const int band_rows = kBand;
+    // Block height: 512 rows; a tall single plane too small to give one wave
+    // of CTAs (148 SMs x 4) halves it down to 128 (a 4096^2 plane: 1024
+    // CTAs).  A function of the image's own size only (not the batch, not a
+    // row band's extent), so batching and aligned row bands never change it.
+    int band_rows = kBand;
+    if (!band_rows) {
+        band_rows = 512;
+        const int himg = g.img_h();
+        while (himg >= 2048 && band_rows > 128 &&
+               strips * ((himg + band_rows - 1) / band_rows) < 148 * 4)
+            band_rows /= 2;
+    }
     const int y0 = g.out_row0, y1 = g.out_row0 + g.height;
     dim3 grid(strips, (y1 - 1) / band_rows - y0 / band_rows + 1, g.batch);
     note_kernel("fast_walk_step");
