@@ -77,12 +77,20 @@ const char* osbf_gpu_last_error(void);
  * tests and the benchmark, no reference counterpart. */
 const char* osbf_gpu_last_kernel(void);
 
-/* Diagnostics: force the kernel family of fast passes process-wide ("strip",
- * "tile", "tma", "stream", "sep"; NULL or "" = per-radius default).  A family
+/* Diagnostics: force the kernel family of fast passes process-wide ("walk",
+ * "tma", "stream", "strip", "tile", "sep", ...; NULL or "" = per-radius default).  A family
  * that does not apply to a pass (radius, layout) falls through to the
  * default order.  No reference counterpart; results stay within fast mode's
  * tolerance whichever family runs. */
 osbf_status osbf_gpu_set_fast_kernel(const char* name);
+/* Largest radius the fast mode serves with a fast kernel: radii up to 16 run
+ * the templated kernels, larger ones the generic vertical-first walk (O(1)
+ * state per thread in r) -- for whole planes up to r = 56, where the exact
+ * whole-table kernels become as fast; above that a fast-mode call runs the
+ * exact kernels (bit-identical, like the reference accepts any r >= 1,
+ * filters2d.hpp:61-63).  Row bands (osbf_gpu_step_band*) accept radii up to
+ * this value.  No reference counterpart; host-only, no device needed. */
+int osbf_gpu_fast_max_radius(void);
 /* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
 int osbf_gpu_device_available(void);
 

@@ -184,9 +184,15 @@ class Context:
     @staticmethod
     def set_fast_kernel(name: str | None) -> None:
         """Diagnostics: force the fast-pass kernel family process-wide
-        (osbf_gpu_set_fast_kernel): "strip", "tile", "tma", "stream", "sep",
+        (osbf_gpu_set_fast_kernel): "walk", "tma", "stream", "strip", "tile", "sep",
         or None for the per-radius default."""
         _check(N.lib().osbf_gpu_set_fast_kernel((name or "").encode()))
+
+    @staticmethod
+    def fast_max_radius() -> int:
+        """Largest radius with a fast kernel (osbf_gpu_fast_max_radius):
+        16 templated radii, then the generic vertical-first walk."""
+        return int(N.lib().osbf_gpu_fast_max_radius())
 
     @property
     def last_kernel(self) -> str:

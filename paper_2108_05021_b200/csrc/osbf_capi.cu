@@ -192,10 +192,26 @@ bool exact_table_forced() {
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
                      int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
                      osbf_mode mode, cudaStream_t s) {
-    // Fast mode has compiled kernels up to kFastMaxRadius; larger windows run
-    // the exact GPU kernels (bit-identical to the reference, hence also
-    // within the fast mode's tolerance), like the reference accepts any r.
-    if (mode == OSBF_MODE_FAST && r > osbf_gpu::kFastMaxRadius) mode = OSBF_MODE_EXACT;
+    // Fast mode: templated kernels up to kFastMaxRadius, the generic
+    // vertical-first walk above it (up to fast_generic_max_radius()); beyond
+    // that, or for the per-pixel diagnostics, the exact GPU kernels
+    // (bit-identical to the reference, hence also within the fast mode's
+    // tolerance), like the reference accepts any r.
+    if (mode == OSBF_MODE_FAST && r > osbf_gpu::kFastMaxRadius) {
+        // (whole planes: the generic walk up to r = 56; past that the exact
+        // whole-table kernels measured as fast, 27 vs 30 ms per 32768^2 pass
+        // at r = 64, and their cost does not grow with r)
+        if (dst && !means && !sel && r <= osbf_gpu::kFastGenericPlaneMaxRadius &&
+            r <= osbf_gpu::fast_generic_max_radius()) {
+            const cudaError_t e =
+                osbf_gpu::fast_generic_step(src, g, r, dst, dp, dpl, s, ctx->lc);
+            if (e != cudaErrorNotSupported) {
+                OSBF_CUDA(e, "fast generic step");
+                return OSBF_OK;
+            }
+        }
+        mode = OSBF_MODE_EXACT;
+    }
     if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius &&
         !exact_table_forced()) {
         // fused exact path: row carries + strip kernel (same bits as below)
@@ -404,6 +420,8 @@ int osbf_gpu_abi_version(void) { return OSBF_GPU_ABI_VERSION; }
 const char* osbf_gpu_last_error(void) { return g_last_error.c_str(); }
 
 const char* osbf_gpu_last_kernel(void) { return g_last_kernel; }
+
+int osbf_gpu_fast_max_radius(void) { return osbf_gpu::fast_generic_max_radius(); }
 
 osbf_status osbf_gpu_set_fast_kernel(const char* name) {
     static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "arms", "stream", "walk", "sep"};
@@ -822,9 +840,9 @@ osbf_status osbf_gpu_step_band_push(osbf_ctx* ctx, osbf_dtype in_dtype, const vo
     if (width < 1 || image_height < 1 || in_rows < 1 || out_rows < 1)
         return fail(OSBF_ERR_INVALID_ARGUMENT, "ImagePlane: dimensions must be >= 1");
     if (radius < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "osbf_step: radius must be >= 1");
-    if (radius > osbf_gpu::kFastMaxRadius)
-        return fail(OSBF_ERR_INVALID_ARGUMENT, "fast mode supports radius <= %d (got %d)",
-                    osbf_gpu::kFastMaxRadius, radius);
+    if (radius > osbf_gpu::fast_generic_max_radius())
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "row bands support radius <= %d (got %d)",
+                    osbf_gpu::fast_generic_max_radius(), radius);
     if (out_row0 < 0 || out_row0 + out_rows > image_height)
         return fail(OSBF_ERR_OUT_OF_RANGE, "output rows [%d, %d) outside the image height %d",
                     out_row0, out_row0 + out_rows, image_height);
@@ -851,6 +869,13 @@ osbf_status osbf_gpu_step_band_push(osbf_ctx* ctx, osbf_dtype in_dtype, const vo
         g.push_pitch = push_pitch;
     }
     const osbf_gpu::PlaneView input{d_in, in_dtype, in_pitch, in_pitch * in_rows};
+    if (radius > osbf_gpu::kFastMaxRadius) {
+        OSBF_CUDA(osbf_gpu::fast_generic_step(input, g, radius, d_out, out_pitch,
+                                              out_pitch * out_rows, pick_stream(ctx, stream),
+                                              ctx->lc),
+                  "band step");
+        return OSBF_OK;
+    }
     OSBF_CUDA(osbf_gpu::fast_step(input, g, radius, d_out, out_pitch, out_pitch * out_rows, nullptr,
                                   nullptr, pick_stream(ctx, stream), ctx->lc),
               "band step");

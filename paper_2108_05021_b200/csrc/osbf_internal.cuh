@@ -138,6 +138,19 @@ cudaError_t fast_step(const PlaneView& in, const Geometry& g, int radius, double
                       size_t out_pitch, size_t out_plane, double* means, uint8_t* sel,
                       cudaStream_t s, LaunchCounter& lc);
 
+// One fast pass for kFastMaxRadius < radius <= fast_generic_max_radius():
+// the vertical-first column walk (osbf_fast_vwalk.cu), O(1) state per thread
+// in r.  cudaErrorNotSupported (nothing launched) when the layout or radius
+// has no kernel.
+cudaError_t fast_generic_step(const PlaneView& in, const Geometry& g, int radius, double* out,
+                              size_t out_pitch, size_t out_plane, cudaStream_t s,
+                              LaunchCounter& lc);
+int fast_generic_max_radius();
+// Whole-plane fast passes use the generic walk up to this radius (crossover
+// with the exact whole-table path, measured); row bands use it up to
+// fast_generic_max_radius() (the exact path cannot be banded).
+constexpr int kFastGenericPlaneMaxRadius = 56;
+
 // k = 2..4 fast passes in one launch (temporal blocking, radius <= 4).
 // Returns cudaErrorNotSupported (nothing launched) when the radius / layout /
 // k has no multi-pass kernel; the caller then runs fewer passes per launch.

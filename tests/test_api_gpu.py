@@ -119,14 +119,18 @@ def test_repeated_calls_replay_a_graph(ctx, oracle_lib, mode):
     assert torch.equal(z, y)
 
 
-def test_fast_mode_large_radius_runs_exact_kernels(ctx, oracle_lib):
-    """The reference accepts any r; fast mode has kernels up to r=16 and runs
-    larger windows on the exact kernels (bit-identical)."""
+def test_fast_mode_beyond_generic_radius_runs_exact_kernels(ctx, oracle_lib):
+    """The reference accepts any r; fast mode has kernels up to
+    Context.fast_max_radius() (templated to 16, then the generic walk) and
+    runs larger windows on the exact kernels (bit-identical)."""
     import torch
 
-    p = np.random.default_rng(3).random((90, 70)) * 255
-    got = ctx.iterate(torch.from_numpy(p).cuda(), 23, 2, mode="fast").cpu().numpy()
-    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 23, 2)))
+    import paper_2108_05021_b200 as ob
+
+    r = ob.Context.fast_max_radius() + 3
+    p = np.random.default_rng(3).random((90, 2 * r + 7)) * 255
+    got = ctx.iterate(torch.from_numpy(p).cuda(), r, 2, mode="fast").cpu().numpy()
+    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, r, 2)))
 
 
 def test_out_argument_is_validated(ctx):
