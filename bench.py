@@ -49,6 +49,7 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
            0x100: "display_clock_setting"}
 IN_BYTES = {"u8": 1, "f32": 4, "f64": 8}
 SWEEP_RADII = (1, 2, 4, 8, 16)
+C5_SWEEP_RADII = (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)  # > 16: the generic walk
 
 
 def parse(argv=None):
@@ -353,9 +354,9 @@ def sub_c4(ctx, steps):
             "ms_per_step": round(step, 4), "roofline": rl, "clocks": c}
 
 
-def sub_sweep(ctx, x, workload, iters, radii, in_bytes, reps=5):
-    """One record per radius, each with its own clocks: ``iters`` fast passes
-    over ``x`` (fp64 storage between passes)."""
+def sub_sweep(ctx, x, workload, iters, radii, in_bytes, reps=5, mode="fast"):
+    """One record per radius, each with its own clocks: ``iters`` passes in
+    ``mode`` over ``x`` (fp64 storage between passes)."""
     import torch
 
     y = torch.empty(x.shape, dtype=torch.float64, device="cuda")
@@ -363,14 +364,14 @@ def sub_sweep(ctx, x, workload, iters, radii, in_bytes, reps=5):
     px = x.numel()
     for r in radii:
         for _ in range(2):
-            ctx.iterate(x, r, iters, mode="fast", out=y)
+            ctx.iterate(x, r, iters, mode=mode, out=y)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.iterate(x, r, iters, mode="fast", out=y)
+        ctx.iterate(x, r, iters, mode=mode, out=y)
         torch.cuda.synchronize()
         n = max(reps, int(0.8 / max(time.perf_counter() - t0, 1e-4)))  # >= ~0.8 s sampled
         clk = ClockSampler(torch.cuda.current_device()).start()
-        ms = time_steps(lambda: ctx.iterate(x, r, iters, mode="fast", out=y), n,
+        ms = time_steps(lambda: ctx.iterate(x, r, iters, mode=mode, out=y), n,
                         torch.cuda.current_stream())
         c = clk.stop()
         step = statistics.median(ms)
@@ -523,13 +524,18 @@ def run_c5(args, world, rank, local):
         xf = x.double()
         subs["r_sweep"] = sub_sweep(ctx, xf, "one fast pass of the 32768^2 C5 plane (fp64 in "
                                     "and out) per radius: the r-flatness check",
-                                    1, SWEEP_RADII, 8)
+                                    1, C5_SWEEP_RADII, 8)
         del xf
         torch.cuda.empty_cache()
         c3 = torch.from_numpy(synth.make_input("C3")[0]).cuda()
         subs["C3"] = sub_sweep(ctx, c3, "C3: 4096^2 uint8, 10 fast iterations per radius "
-                               "(plane fits L2: per-pass figure is not an HBM bound)",
-                               10, SWEEP_RADII, 1)
+                               "(first pass bit-exact; plane fits L2: per-pass figure is not "
+                               "an HBM bound)", 10, SWEEP_RADII, 1)
+        # the mode that is bit-exact over all 10 iterations (C3's parity bar:
+        # tests/test_configs_gpu.py::test_c3_full_exact_bit_exact)
+        subs["C3_exact"] = sub_sweep(ctx, c3, "C3: 4096^2 uint8, 10 exact iterations per "
+                                     "radius (bit-identical to the reference at every "
+                                     "iteration)", 10, SWEEP_RADII, 1, reps=3, mode="exact")
         result["sub"] = subs
 
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
