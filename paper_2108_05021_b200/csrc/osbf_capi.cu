@@ -179,14 +179,18 @@ int tb_env() {
     return k;
 }
 
-// OSBF_GPU_EXACT=table: every exact pass on the whole-table path (A/B runs).
-bool exact_table_forced() {
-    static const bool on = [] {
-        const char* v = std::getenv("OSBF_GPU_EXACT");
-        return v && std::strcmp(v, "table") == 0;
+// OSBF_GPU_EXACT=table / strip: every exact pass on the whole-table path, or
+// on the fused strip walk whenever its radius allows (A/B runs and tests of
+// the path a launch would not pick by default).
+const char* exact_forced() {
+    static const char* v = [] {
+        const char* e = std::getenv("OSBF_GPU_EXACT");
+        return e ? e : "";
     }();
-    return on;
+    return v;
 }
+bool exact_table_forced() { return std::strcmp(exact_forced(), "table") == 0; }
+bool exact_strip_forced() { return std::strcmp(exact_forced(), "strip") == 0; }
 
 // One pass in the requested mode: src (typed view) -> dst (fp64).
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
@@ -213,7 +217,7 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
         mode = OSBF_MODE_EXACT;
     }
     if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius &&
-        !exact_table_forced()) {
+        !exact_table_forced() && (exact_strip_forced() || !osbf_gpu::exact_prefers_table(g))) {
         // fused exact path: row carries + strip kernel (same bits as below)
         OSBF_CUDA(ctx->rowpfx.ensure(osbf_gpu::exact_fused_carry_elems(g) * sizeof(double)),
                   "alloc carries");

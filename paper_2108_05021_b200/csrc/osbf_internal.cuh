@@ -93,6 +93,10 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
 // Bit-identical to exact_build_sat + exact_select; radius <= kExactFusedMaxRadius.
 constexpr int kExactFusedMaxRadius = 16;
 size_t exact_fused_carry_elems(const Geometry& g);
+// Few strips x planes (one 4096^2 plane: 128): the fused strip walk cannot
+// fill the device, and the whole-table path (deep-prefetch serial chains +
+// a fully parallel stencil) is faster -- same table, same bits.
+bool exact_prefers_table(const Geometry& g);
 cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius, double* carries,
                              double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
                              LaunchCounter& lc);

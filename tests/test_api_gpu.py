@@ -59,7 +59,14 @@ def test_launch_counter_counts_kernels(ctx):
     x = torch.rand((64, 64), dtype=torch.float64, device="cuda")
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="exact")
-    assert ctx.launches - before == 6  # 2 kernels per exact pass (row carries + strip)
+    # a lone small plane: the whole-table path, 3 kernels per exact pass
+    # (row prefixes, column chains, stencil)
+    assert ctx.launches - before == 9 and "exact_col_chain" in ctx.last_kernel
+    xb = torch.rand((300, 64, 64), dtype=torch.float64, device="cuda")
+    before = ctx.launches
+    ctx.iterate(xb, 2, 3, mode="exact")
+    # enough strips x planes for the fused walk: 2 kernels per pass (row carries + strip)
+    assert ctx.launches - before == 6 and "exact_strip" in ctx.last_kernel
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="fast")
     assert ctx.launches - before == 3
