@@ -15,6 +15,7 @@
 //                         order, write a_m itself (filters2d.hpp:80-83).
 // All fp64 arithmetic uses the _rn intrinsics so nothing is contracted.
 #include <atomic>
+#include <utility>
 
 #include "osbf_exact2_kernel.cuh"
 #include "osbf_internal.cuh"
@@ -308,15 +309,21 @@ __global__ void __launch_bounds__(96)
             mb_arrive(&empty[q]);
             const int nk = min(COL_ROWS, H - st * COL_ROWS);
             if (cx <= W) {
+                if (nk == COL_ROWS) {  // full stage: straight-line stores
 #pragma unroll
-                for (int k = 0; k < COL_ROWS; ++k) {
-                    if (k < nk) {
+                    for (int k = 0; k < COL_ROWS; ++k) {
                         unsafe |= !table_value_safe(v[k]);
-                        cp[k * cols] = v[k];
+                        *cp = v[k];
+                        cp += cols;
+                    }
+                } else {
+                    for (int k = 0; k < nk; ++k) {
+                        unsafe |= !table_value_safe(v[k]);
+                        *cp = v[k];
+                        cp += cols;
                     }
                 }
             }
-            cp += COL_ROWS * cols;
         }
         flag_unsafe(unsafe);
     }
@@ -324,13 +331,17 @@ __global__ void __launch_bounds__(96)
 
 // C / cols: the table of plane b (or a shared-memory copy of the part this
 // pixel reads: C then points at the copy's virtual origin, cols is its pitch).
-template <typename T>
+// RT > 0: the radius as a compile-time constant (corner offsets become
+// immediates); ro1..ro3 = r, r+1, 2r+1 table rows, precomputed per thread.
+template <typename T, int RT>
 __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_pitch,
                                            size_t in_plane, const double* C, long long cols,
                                            double* __restrict__ out, size_t out_pitch,
                                            size_t out_plane, double* __restrict__ means,
-                                           uint8_t* __restrict__ sel, int W, int H, int r, int x,
-                                           int y, int b, bool safe, double yq, double yh) {
+                                           uint8_t* __restrict__ sel, int W, int H, int r_rt,
+                                           int x, int y, int b, bool safe, double yq, double yh,
+                                           int ro1, int ro2, int ro3) {
+    const int r = RT > 0 ? RT : r_rt;
     if (x >= W || y >= H) return;
     const double u = to_f64(in[b * in_plane + static_cast<size_t>(y) * in_pitch + x]);
     const bool diag = means != nullptr || sel != nullptr;
@@ -342,8 +353,7 @@ __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_p
         // one 64-bit base, then 32-bit row / column offsets (a table row of
         // W+1 doubles; (2r+1) rows of it fit an int for any plane we accept)
         const double* p0 = C + static_cast<long long>(y - r) * cols + (x - r);
-        const int ic = static_cast<int>(cols);
-        const int ro[4] = {0, r * ic, (r + 1) * ic, (2 * r + 1) * ic};
+        const int ro[4] = {0, ro1, ro2, ro3};
         const int co[4] = {0, r, r + 1, 2 * r + 1};
         double g[4][4];
 #pragma unroll
@@ -370,8 +380,14 @@ __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_p
             dv[i] = fabs(__dsub_rn(av[i], u));
         }
         double best = 0.0;
-        const double dsum = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
-        if (fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL)) {
+        // a safe table (finite, in range) gives finite d_i; otherwise check
+        bool finite = safe;
+        if (!safe) {
+            const double dsum =
+                ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
+            finite = fabs(dsum) < __longlong_as_double(0x7ff0000000000000LL);
+        }
+        if (finite) {
             // all |a_i - u| finite: a stable depth-3 tournament returns the
             // first minimum, the reference's strict < (filters2d.hpp:78)
             auto pick = [](double& d0, double& a0, double d1, double a1) {
@@ -429,23 +445,46 @@ __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_p
 
 constexpr int kStencilRows = 4;  // rows per thread (block: 32 x 8 threads, 32 x 32 pixels)
 
-template <typename T>
+template <typename T, int RT>
 __global__ void __launch_bounds__(256)
     exact_stencil(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
                   const double* __restrict__ sat, double* __restrict__ out, size_t out_pitch,
                   size_t out_plane, double* __restrict__ means, uint8_t* __restrict__ sel, int W,
-                  int H, int r, double yq, double yh) {
+                  int H, int r_rt, double yq, double yh) {
+    const int r = RT > 0 ? RT : r_rt;
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const int b = blockIdx.z;
     const bool safe = *reinterpret_cast<volatile unsigned*>(&g_table_unsafe) == 0u;
     const long long cols = static_cast<long long>(W) + 1;
     const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
+    const int ic = static_cast<int>(cols);
+    const int ro1 = r * ic, ro2 = (r + 1) * ic, ro3 = (2 * r + 1) * ic;
 #pragma unroll 1
     for (int k = 0; k < kStencilRows; ++k) {
         const int y = blockIdx.y * (8 * kStencilRows) + (threadIdx.x >> 5) + 8 * k;
-        stencil_px<T>(in, in_pitch, in_plane, C, cols, out, out_pitch, out_plane, means, sel, W,
-                      H, r, x, y, b, safe, yq, yh);
+        stencil_px<T, RT>(in, in_pitch, in_plane, C, cols, out, out_pitch, out_plane, means, sel,
+                          W, H, r, x, y, b, safe, yq, yh, ro1, ro2, ro3);
     }
+}
+
+template <typename T, int RT>
+void launch_stencil_rt(dim3 grid, cudaStream_t s, const T* in, size_t ip, size_t ipl,
+                       const double* sat, double* out, size_t op, size_t opl, int W, int H, int r,
+                       double yq, double yh) {
+    exact_stencil<T, RT><<<grid, 256, 0, s>>>(in, ip, ipl, sat, out, op, opl, nullptr, nullptr, W,
+                                              H, r, yq, yh);
+}
+template <typename T, int... Rs>
+bool launch_stencil_fixed(std::integer_sequence<int, Rs...>, dim3 grid, cudaStream_t s,
+                          const T* in, size_t ip, size_t ipl, const double* sat, double* out,
+                          size_t op, size_t opl, int W, int H, int r, double yq, double yh) {
+    bool hit = false;
+    ((r == Rs + 1 ? (launch_stencil_rt<T, Rs + 1>(grid, s, in, ip, ipl, sat, out, op, opl, W, H,
+                                                  r, yq, yh),
+                     hit = true)
+                  : false),
+     ...);
+    return hit;
 }
 
 template <typename T>
@@ -468,8 +507,18 @@ cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const 
     // interior reciprocals RN(1/n) (IEEE on the host, the same value)
     const double yq = 1.0 / static_cast<double>((r + 1) * (r + 1));
     const double yh = 1.0 / static_cast<double>((r + 1) * (2 * r + 1));
-    exact_stencil<T><<<grid, 256, 0, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane, sat,
-                                          out, op, opl, means, sel, g.width, g.height, r, yq, yh);
+    // fp64 planes (every pass after the first), no diagnostics, r <= 16: the
+    // radius as a template constant
+    if constexpr (sizeof(T) == 8) {
+        if (!means && !sel && out &&
+            launch_stencil_fixed<T>(std::make_integer_sequence<int, 16>{}, grid, s,
+                                    static_cast<const T*>(in.base), in.pitch, in.plane, sat, out,
+                                    op, opl, g.width, g.height, r, yq, yh))
+            return cudaGetLastError();
+    }
+    exact_stencil<T, 0><<<grid, 256, 0, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane,
+                                             sat, out, op, opl, means, sel, g.width, g.height, r,
+                                             yq, yh);
     return cudaGetLastError();
 }
 

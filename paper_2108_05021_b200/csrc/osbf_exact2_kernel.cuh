@@ -57,8 +57,11 @@ __device__ __forceinline__ double div_by_count(double s, double n, double y) {
 // window sum ((A-B)-C)+D of safe values is 0 or a multiple of 2^-852 below
 // 2^902, so div_by_count_unguarded is exact for it.
 __device__ __forceinline__ bool table_value_safe(double v) {
-    const unsigned e = static_cast<unsigned>(__double2hiint(v)) & 0x7ff00000u;
-    return v == 0.0 || (e - (223u << 20)) <= ((1923u - 223u) << 20);
+    // integer-only: |v| == 0 or its exponent in [223, 1923] (no fp64 compare)
+    const unsigned hi = static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu;
+    const unsigned lo = static_cast<unsigned>(__double2loint(v));
+    const unsigned e = hi & 0x7ff00000u;
+    return ((hi | lo) == 0u) | ((e - (223u << 20)) <= ((1923u - 223u) << 20));
 }
 
 namespace ex2 {

@@ -385,3 +385,24 @@ def test_temporal_blocking_matches_single_passes(oracle_lib, r, k):
     assert np.mean(np.abs(tb - single) > 1e-9 * 255.0) < 0.02
     ctxk.iterate(torch_dev(u8), r, 1, mode="fast")  # one pass: single kernel, exact
     ctxk.close()
+
+
+@pytest.mark.parametrize("shape", [(200, 180), (100, 40, 96)])
+def test_exact_non_finite_samples_bit_exact(ctx, oracle_lib, shape):
+    """NaN / inf samples propagate through the reference's table exactly as
+    its serial adds do; exact mode (table path for a lone plane, the strip
+    walk for batches) matches the oracle bit for bit, NaN positions
+    included.  Also raises the table-range flag, after which the stencil
+    keeps its guarded division."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    p = rng.random(shape) * 50.0
+    flat = p.reshape(-1)
+    flat[rng.integers(0, flat.size, 5)] = np.nan
+    flat[rng.integers(0, flat.size, 3)] = np.inf
+    flat[rng.integers(0, flat.size, 2)] = -np.inf
+    got = ctx.iterate(torch.from_numpy(p).cuda(), 3, 2, mode="exact").cpu().numpy()
+    planes = p.reshape((-1,) + p.shape[-2:])
+    want = np.stack([oracle_lib.osbf(c, 3, 2) for c in planes]).reshape(p.shape)
+    assert np.array_equal(bits(got), bits(want))
