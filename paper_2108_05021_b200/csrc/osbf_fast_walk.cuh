@@ -39,7 +39,8 @@ struct WLay {
     static constexpr int SW = 128;
     static constexpr int NSEG = 8;   // arm segments per row
     static constexpr int L = 2 * R + 2;  // register ring length
-    // rows per chunk: a multiple of L (R <= 5) or L / 2 (NP = 2 ring phases)
+    // rows per chunk: a multiple of L (R <= 5) or L / 2 (NP = 2 ring phases;
+    // keeps 4 CTAs per SM in shared memory at r = 6)
     static constexpr int CH = R == 1 ? 8 : (R <= 5 ? L : L / 2);
     static constexpr int NP = (CH % L == 0) ? 1 : L / CH;
     static_assert(CH % L == 0 || L % CH == 0, "chunk / ring");
@@ -61,8 +62,10 @@ struct WLay {
     // the last segment of a row may read up to LS + R + XOFF elements past
     // the row's useful part (feeding unused arms only)
     static constexpr size_t PAD = ((LS + R + XOFF) * sizeof(T) + 127) / 128 * 128;
-    // register budget: 4 CTAs per SM up to r = 4, 3 to r = 8, then 2
-    static constexpr int MINB = R <= 4 ? 4 : (R <= 8 ? 3 : 2);
+    // register budget: 4 CTAs per SM up to r = 4 and at r = 6 (128 registers,
+    // no spills; r = 5 keeps its 12-row chunks at 3 CTAs: measured faster),
+    // 3 to r = 8, then 2
+    static constexpr int MINB = (R <= 4 || R == 6) ? 4 : (R <= 8 ? 3 : 2);
     static constexpr size_t kCtaSmem = (MINB == 4 ? 56 : MINB == 3 ? 74 : 112) * 1024;
     static constexpr size_t H_BYTES = 2 * H_ELEMS * sizeof(double);
     static constexpr int NU_FIT =
