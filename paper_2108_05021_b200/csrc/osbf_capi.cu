@@ -192,6 +192,19 @@ const char* exact_forced() {
 bool exact_table_forced() { return std::strcmp(exact_forced(), "table") == 0; }
 bool exact_strip_forced() { return std::strcmp(exact_forced(), "strip") == 0; }
 
+// The fast-pass family forced by osbf_gpu_set_fast_kernel or OSBF_GPU_FAST.
+bool fast_family_forced(const char* name) {
+    const char* o = osbf_gpu::fast_kernel_override();
+    if (!o) {
+        static const char* env = [] {
+            const char* e = std::getenv("OSBF_GPU_FAST");
+            return e ? e : "";
+        }();
+        o = env;
+    }
+    return std::strcmp(o, name) == 0;
+}
+
 // One pass in the requested mode: src (typed view) -> dst (fp64).
 osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_gpu::Geometry& g,
                      int r, double* dst, size_t dp, size_t dpl, double* means, uint8_t* sel,
@@ -205,8 +218,11 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
         // (whole planes: the generic walk up to r = 56; past that the exact
         // whole-table kernels measured as fast, 27 vs 30 ms per 32768^2 pass
         // at r = 64, and their cost does not grow with r)
-        if (dst && !means && !sel && r <= osbf_gpu::kFastGenericPlaneMaxRadius &&
-            r <= osbf_gpu::fast_generic_max_radius()) {
+        // (OSBF_GPU_FAST / osbf_gpu_set_fast_kernel "vwalk": always, for tests)
+        const bool forced = fast_family_forced("vwalk");
+        if (dst && !means && !sel && r <= osbf_gpu::fast_generic_max_radius() &&
+            (forced || (r <= osbf_gpu::kFastGenericPlaneMaxRadius &&
+                        osbf_gpu::fast_generic_fills(g, r)))) {
             const cudaError_t e =
                 osbf_gpu::fast_generic_step(src, g, r, dst, dp, dpl, s, ctx->lc);
             if (e != cudaErrorNotSupported) {
@@ -428,7 +444,7 @@ const char* osbf_gpu_last_kernel(void) { return g_last_kernel; }
 int osbf_gpu_fast_max_radius(void) { return osbf_gpu::fast_generic_max_radius(); }
 
 osbf_status osbf_gpu_set_fast_kernel(const char* name) {
-    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "arms", "stream", "walk", "sep"};
+    static const char* const kNames[] = {"strip", "tile", "tma", "tmaseq", "tmaint", "pair", "arms", "stream", "walk", "vwalk", "sep"};
     if (!name || !name[0]) {
         osbf_gpu::g_fast_override.store(nullptr, std::memory_order_release);
         return OSBF_OK;

@@ -1272,7 +1272,7 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
         }
     }
     if constexpr (R <= kWalkMaxRadius && !DIAG) {
-        if (fast_allowed("walk", R >= 3)) {
+        if (fast_allowed("walk", R >= 3 && walk_fills(g))) {
             cudaError_t e = cudaErrorNotSupported;
             switch (in.dtype) {
                 case OSBF_U8: e = launch_walk<R, uint8_t, true>(in, g, out, op, opl, s); break;
@@ -1283,7 +1283,8 @@ cudaError_t launch_dtype(const PlaneView& in, const Geometry& g, double* out, si
         }
     }
     if constexpr (R >= kStreamMinRadius && R <= kStreamMaxRadius && !DIAG) {
-        if (stream_enabled() && fast_allowed("stream", true)) {
+        // superseded by the walk (kept as a selectable family for A/B runs)
+        if (stream_enabled() && fast_allowed("stream", false)) {
             cudaError_t e = cudaErrorNotSupported;
             switch (in.dtype) {
                 case OSBF_U8: e = launch_stream<R, uint8_t, true>(in, g, out, op, opl, s); break;

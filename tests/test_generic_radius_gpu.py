@@ -18,8 +18,19 @@ def test_generic_max_radius_host_query():
     assert ob.Context.fast_max_radius() >= 64
 
 
+@pytest.fixture
+def vwalk():
+    """Small test planes would not fill one wave of CTAs, where whole-plane
+    calls prefer the exact path: force the generic walk."""
+    import paper_2108_05021_b200 as ob
+
+    ob.Context.set_fast_kernel("vwalk")
+    yield
+    ob.Context.set_fast_kernel(None)
+
+
 @pytest.mark.parametrize("r", [17, 20, 24, 32, 47, 56])
-def test_generic_radius_matches_oracle(ctx, oracle_lib, r):
+def test_generic_radius_matches_oracle(ctx, oracle_lib, vwalk, r):
     import torch
     rng = np.random.default_rng(1700 + r)
     for shape in [(1, 3, 2), (1, r, 2 * r + 1), (2, 37, 300), (1, 700, 129), (1, 530, 611)]:
@@ -38,7 +49,7 @@ def test_generic_radius_matches_oracle(ctx, oracle_lib, r):
     assert float(np.abs(got[0] - want).max()) <= FLOAT_TOL * 8.0
 
 
-def test_generic_radius_tall_image_blocks(ctx, oracle_lib):
+def test_generic_radius_tall_image_blocks(ctx, oracle_lib, vwalk):
     """Several 512-row blocks per strip and several strips (block seams)."""
     import torch
 
@@ -50,7 +61,7 @@ def test_generic_radius_tall_image_blocks(ctx, oracle_lib):
 
 
 @pytest.mark.parametrize("r", [20, 40])
-def test_generic_radius_row_bands(ctx, r):
+def test_generic_radius_row_bands(ctx, vwalk, r):
     """Row bands on the 512-row block grid are bit-identical to the whole
     image; other cuts agree to fp64 rounding."""
     import torch
@@ -106,3 +117,24 @@ def test_beyond_generic_radius_runs_exact(ctx, oracle_lib):
     got = ctx.iterate(torch.from_numpy(p).cuda(), r, 2, mode="fast").cpu().numpy()
     assert "exact" in ctx.last_kernel
     assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, r, 2)))
+
+
+def test_small_plane_prefers_exact_over_generic_walk(ctx, oracle_lib):
+    """A whole plane too small to give the generic walk one wave runs the
+    exact kernels (bit-identical) instead."""
+    import torch
+
+    p = np.random.default_rng(8).random((300, 260)) * 10.0
+    got = ctx.iterate(torch.from_numpy(p).cuda(), 20, 2, mode="fast").cpu().numpy()
+    assert "exact" in ctx.last_kernel
+    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 20, 2)))
+
+
+def test_large_plane_runs_generic_walk(ctx, oracle_lib):
+    import torch
+
+    p = np.random.default_rng(9).random((8192, 8192)) * 10.0  # 64 strips x 16 blocks
+    got = ctx.iterate(torch.from_numpy(p).cuda(), 20, 1, mode="fast").cpu().numpy()
+    assert ctx.last_kernel == "fast_vwalk_step"
+    want = oracle_lib.osbf(p, 20, 1, threads=8)
+    assert float(np.abs(got - want).max()) <= FLOAT_TOL * 10.0
