@@ -129,6 +129,10 @@ osbf_status check_geometry(int width, int height, int batch) {
     if (width < 1 || height < 1)
         return fail(OSBF_ERR_INVALID_ARGUMENT, "ImagePlane: dimensions must be >= 1");
     if (batch < 1) return fail(OSBF_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+    // the kernels put the plane index in gridDim.z
+    if (batch > 65535)
+        return fail(OSBF_ERR_INVALID_ARGUMENT, "batch must be <= 65535 planes per call (got %d)",
+                    batch);
     return OSBF_OK;
 }
 

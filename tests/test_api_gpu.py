@@ -208,3 +208,15 @@ def test_band_pass_odd_width_unaligned_cuts(ctx, oracle_lib, w):
         src = p[i0:i1].clone()  # a tight buffer: nothing past its last row
         ctx.step_band(src, i0, out[a:b], a, b - a, H, r)
     assert float((out - whole).abs().max()) <= 1e-9
+
+
+def test_batch_above_grid_limit_is_rejected(ctx):
+    """Planes ride in gridDim.z: a batch above 65535 is refused up front
+    (InvalidArgument), not failed at launch."""
+    import torch
+
+    import paper_2108_05021_b200 as ob
+
+    x = torch.rand((65536, 2, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(ob.InvalidArgument):
+        ctx.iterate(x, 1, 1, mode="fast")
