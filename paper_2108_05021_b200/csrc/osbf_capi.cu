@@ -246,14 +246,16 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
                   "exact fused step");
     } else if (mode == OSBF_MODE_EXACT) {
         const size_t n = static_cast<size_t>(g.batch) * g.width * g.height;
-        const size_t ns = static_cast<size_t>(g.batch) * (g.width + 1) * (g.height + 1);
+        // even table pitch: 16-byte rows, so the stencil walk can stage them with TMA
+        const size_t tp = (static_cast<size_t>(g.width) + 2) & ~static_cast<size_t>(1);
+        const size_t ns = static_cast<size_t>(g.batch) * tp * (g.height + 1);
         OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");
         OSBF_CUDA(ctx->sat.ensure(ns * sizeof(double)), "alloc sat");
         OSBF_CUDA(osbf_gpu::exact_build_sat(src, g, ctx->rowpfx.as<double>(), ctx->sat.as<double>(),
-                                            s, ctx->lc),
+                                            s, ctx->lc, tp),
                   "exact SAT");
         OSBF_CUDA(osbf_gpu::exact_select(src, g, r, ctx->sat.as<double>(), dst, dp, dpl, means, sel,
-                                         s, ctx->lc),
+                                         s, ctx->lc, tp),
                   "exact select");
     } else {
         OSBF_CUDA(osbf_gpu::fast_step(src, g, r, dst, dp, dpl, means, sel, s, ctx->lc),

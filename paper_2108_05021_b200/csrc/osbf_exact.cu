@@ -15,6 +15,7 @@
 //                         order, write a_m itself (filters2d.hpp:80-83).
 // All fp64 arithmetic uses the _rn intrinsics so nothing is contracted.
 #include <atomic>
+#include <cstdlib>
 #include <utility>
 
 #include "osbf_exact2_kernel.cuh"
@@ -85,16 +86,16 @@ __device__ __forceinline__ void flag_unsafe(bool unsafe) {
 
 // One thread per table column cx in [0, W] of each plane.
 __global__ void exact_col_chain(const double* __restrict__ rowpfx, double* __restrict__ sat,
-                                int W, int H, int B) {
+                                int W, int H, int B, long long tp) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long cols = static_cast<long long>(W) + 1;
     if (t >= cols * B) return;
     const long long b = t / cols;
     const int cx = static_cast<int>(t - b * cols);
-    double* C = sat + b * cols * (H + 1);
+    double* C = sat + b * tp * (H + 1);
     C[cx] = 0.0;  // zero border row
     if (cx == 0) {
-        for (int cy = 1; cy <= H; ++cy) C[static_cast<long long>(cy) * cols] = 0.0;
+        for (int cy = 1; cy <= H; ++cy) C[static_cast<long long>(cy) * tp] = 0.0;
         return;
     }
     const double* R = rowpfx + b * static_cast<long long>(W) * H + (cx - 1);
@@ -104,7 +105,7 @@ __global__ void exact_col_chain(const double* __restrict__ rowpfx, double* __res
     for (int y = 0; y < H; ++y) {
         acc = __dadd_rn(acc, R[static_cast<long long>(y) * W]);  // above[x+1] + row (integral.hpp:26)
         unsafe |= !table_value_safe(acc);
-        C[static_cast<long long>(y + 1) * cols + cx] = acc;
+        C[static_cast<long long>(y + 1) * tp + cx] = acc;
     }
     if (unsafe) atomicOr(&g_table_unsafe, 1u);
 }
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(96)
 // only load / add / store per element.
 __global__ void __launch_bounds__(96)
     exact_col_chain_deep(const double* __restrict__ rowpfx, double* __restrict__ sat, int W,
-                         int H, int B) {
+                         int H, int B, long long tp) {
     extern __shared__ double cring[];
     __shared__ uint64_t full[COL_STAGES], done[COL_STAGES], empty[COL_STAGES];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -295,10 +296,10 @@ __global__ void __launch_bounds__(96)
             mb_arrive(&done[q]);
         }
     } else {
-        double* C = sat + static_cast<long long>(b) * cols * (H + 1);
+        double* C = sat + static_cast<long long>(b) * tp * (H + 1);
         if (cx <= W) C[cx] = 0.0;  // zero border row
         bool unsafe = false;
-        double* cp = C + cols + cx;  // table row 1
+        double* cp = C + tp + cx;  // table row 1
         for (int st = 0; st < nst; ++st) {
             const int q = st % COL_STAGES;
             mb_wait(&done[q], (st / COL_STAGES) & 1);
@@ -314,13 +315,13 @@ __global__ void __launch_bounds__(96)
                     for (int k = 0; k < COL_ROWS; ++k) {
                         unsafe |= !table_value_safe(v[k]);
                         *cp = v[k];
-                        cp += cols;
+                        cp += tp;
                     }
                 } else {
                     for (int k = 0; k < nk; ++k) {
                         unsafe |= !table_value_safe(v[k]);
                         *cp = v[k];
-                        cp += cols;
+                        cp += tp;
                     }
                 }
             }
@@ -450,12 +451,11 @@ __global__ void __launch_bounds__(256)
     exact_stencil(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
                   const double* __restrict__ sat, double* __restrict__ out, size_t out_pitch,
                   size_t out_plane, double* __restrict__ means, uint8_t* __restrict__ sel, int W,
-                  int H, int r_rt, double yq, double yh) {
+                  int H, int r_rt, double yq, double yh, long long cols) {
     const int r = RT > 0 ? RT : r_rt;
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const int b = blockIdx.z;
     const bool safe = *reinterpret_cast<volatile unsigned*>(&g_table_unsafe) == 0u;
-    const long long cols = static_cast<long long>(W) + 1;
     const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
     const int ic = static_cast<int>(cols);
     const int ro1 = r * ic, ro2 = (r + 1) * ic, ro3 = (2 * r + 1) * ic;
@@ -470,17 +470,18 @@ __global__ void __launch_bounds__(256)
 template <typename T, int RT>
 void launch_stencil_rt(dim3 grid, cudaStream_t s, const T* in, size_t ip, size_t ipl,
                        const double* sat, double* out, size_t op, size_t opl, int W, int H, int r,
-                       double yq, double yh) {
+                       double yq, double yh, long long tp) {
     exact_stencil<T, RT><<<grid, 256, 0, s>>>(in, ip, ipl, sat, out, op, opl, nullptr, nullptr, W,
-                                              H, r, yq, yh);
+                                              H, r, yq, yh, tp);
 }
 template <typename T, int... Rs>
 bool launch_stencil_fixed(std::integer_sequence<int, Rs...>, dim3 grid, cudaStream_t s,
                           const T* in, size_t ip, size_t ipl, const double* sat, double* out,
-                          size_t op, size_t opl, int W, int H, int r, double yq, double yh) {
+                          size_t op, size_t opl, int W, int H, int r, double yq, double yh,
+                          long long tp) {
     bool hit = false;
     ((r == Rs + 1 ? (launch_stencil_rt<T, Rs + 1>(grid, s, in, ip, ipl, sat, out, op, opl, W, H,
-                                                  r, yq, yh),
+                                                  r, yq, yh, tp),
                      hit = true)
                   : false),
      ...);
@@ -501,7 +502,7 @@ cudaError_t launch_row_prefix(const PlaneView& in, const Geometry& g, double* ro
 template <typename T>
 cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const double* sat,
                            double* out, size_t op, size_t opl, double* means, uint8_t* sel,
-                           cudaStream_t s) {
+                           cudaStream_t s, long long tp) {
     dim3 grid((g.width + 31) / 32, (g.height + 8 * kStencilRows - 1) / (8 * kStencilRows),
               g.batch);
     // interior reciprocals RN(1/n) (IEEE on the host, the same value)
@@ -513,12 +514,12 @@ cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const 
         if (!means && !sel && out &&
             launch_stencil_fixed<T>(std::make_integer_sequence<int, 16>{}, grid, s,
                                     static_cast<const T*>(in.base), in.pitch, in.plane, sat, out,
-                                    op, opl, g.width, g.height, r, yq, yh))
+                                    op, opl, g.width, g.height, r, yq, yh, tp))
             return cudaGetLastError();
     }
     exact_stencil<T, 0><<<grid, 256, 0, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane,
                                              sat, out, op, opl, means, sel, g.width, g.height, r,
-                                             yq, yh);
+                                             yq, yh, tp);
     return cudaGetLastError();
 }
 
@@ -543,7 +544,8 @@ bool table_deep(const Geometry& g) {
 }
 
 cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
-                            cudaStream_t s, LaunchCounter& lc) {
+                            cudaStream_t s, LaunchCounter& lc, size_t tpitch) {
+    const long long tp = tpitch ? static_cast<long long>(tpitch) : g.width + 1LL;
     cudaError_t e;
     if (table_deep(g)) {
         switch (in.dtype) {
@@ -557,7 +559,7 @@ cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowp
         if ((e = ensure_smem(exact_col_chain_deep, COL2_SMEM, done)) != cudaSuccess) return e;
         const long long wpp = (static_cast<long long>(g.width) + 1 + 31) / 32;
         exact_col_chain_deep<<<static_cast<unsigned>(wpp * g.batch), 96, COL2_SMEM, s>>>(
-            rowpfx, sat, g.width, g.height, g.batch);
+            rowpfx, sat, g.width, g.height, g.batch, tp);
         ++lc.launches;
         return cudaGetLastError();
     }
@@ -570,26 +572,66 @@ cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowp
     if (e != cudaSuccess) return e;
     const long long threads = (static_cast<long long>(g.width) + 1) * g.batch;
     exact_col_chain<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(
-        rowpfx, sat, g.width, g.height, g.batch);
+        rowpfx, sat, g.width, g.height, g.batch, tp);
     ++lc.launches;
     return cudaGetLastError();
 }
 
+namespace {
+using TwalkFn = cudaError_t (*)(const PlaneView&, const Geometry&, const double*, size_t, double*,
+                                size_t, size_t, const unsigned*, cudaStream_t);
+constexpr TwalkFn kTwalk[kExactFusedMaxRadius + 1] = {
+    nullptr,
+    exact_twalk_launch<1>,  exact_twalk_launch<2>,  exact_twalk_launch<3>,
+    exact_twalk_launch<4>,  exact_twalk_launch<5>,  exact_twalk_launch<6>,
+    exact_twalk_launch<7>,  exact_twalk_launch<8>,  exact_twalk_launch<9>,
+    exact_twalk_launch<10>, exact_twalk_launch<11>, exact_twalk_launch<12>,
+    exact_twalk_launch<13>, exact_twalk_launch<14>, exact_twalk_launch<15>,
+    exact_twalk_launch<16>,
+};
+
+// OSBF_GPU_TWALK=0: keep the per-thread corner-load stencil (A/B runs, tests).
+bool twalk_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("OSBF_GPU_TWALK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
+
 cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
                          double* out, size_t out_pitch, size_t out_plane, double* means,
-                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc) {
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch) {
     ++lc.launches;
+    const long long tp = tpitch ? static_cast<long long>(tpitch) : g.width + 1LL;
+    if (out && !means && !sel && radius <= kExactFusedMaxRadius && twalk_enabled()) {
+        static unsigned* flag = [] {
+            void* p = nullptr;
+            return cudaGetSymbolAddress(&p, g_table_unsafe) == cudaSuccess
+                       ? static_cast<unsigned*>(p)
+                       : nullptr;
+        }();
+        if (flag) {
+            const cudaError_t e = kTwalk[radius](in, g, sat, static_cast<size_t>(tp), out,
+                                                 out_pitch, out_plane, flag, s);
+            if (e != cudaErrorNotSupported) {
+                note_kernel("exact_row_prefix+exact_col_chain+exact_twalk");
+                return e;
+            }
+        }
+    }
     note_kernel("exact_row_prefix+exact_col_chain+exact_select");
     switch (in.dtype) {
         case OSBF_U8:
             return launch_stencil<uint8_t>(in, g, radius, sat, out, out_pitch, out_plane, means,
-                                           sel, s);
+                                           sel, s, tp);
         case OSBF_F32:
             return launch_stencil<float>(in, g, radius, sat, out, out_pitch, out_plane, means, sel,
-                                         s);
+                                         s, tp);
         default:
             return launch_stencil<double>(in, g, radius, sat, out, out_pitch, out_plane, means,
-                                          sel, s);
+                                          sel, s, tp);
     }
 }
 

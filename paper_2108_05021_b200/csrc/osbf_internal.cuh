@@ -79,15 +79,25 @@ struct LaunchCounter {
 // Whole-image summed-area table in the reference's serial order.
 //   rowpfx: fp64 [batch][height][width] workspace (row running sums)
 //   sat   : fp64 [batch][height+1][width+1]
+//   tpitch: table row pitch in doubles (0 = width+1; the osbf pass path uses
+//           an even pitch so the stencil walk can stage table rows with TMA)
 cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
-                            cudaStream_t s, LaunchCounter& lc);
+                            cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0);
 // One exact OSBF pass reading `in` and the SAT built from it.
 //   out   : fp64 (nullable), out_pitch / out_plane in elements
 //   means : fp64 [batch][height][width][8] (nullable)
 //   sel   : uint8 [batch][height][width] (nullable)
 cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
                          double* out, size_t out_pitch, size_t out_plane, double* means,
-                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc);
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0);
+
+// Table-path stencil as a TMA-staged column walk (osbf_exact_twalk.cuh,
+// instantiated per radius in osbf_exact2_rNN.cu); cudaErrorNotSupported
+// (nothing launched) when the table / input layout is not TMA-able.
+template <int R>
+cudaError_t exact_twalk_launch(const PlaneView& in, const Geometry& g, const double* sat,
+                               size_t tpitch, double* out, size_t op, size_t opl,
+                               const unsigned* unsafe_flag, cudaStream_t s);
 
 // Fused exact path (osbf_exact2_kernel.cuh): row carries + strip kernel.
 // Bit-identical to exact_build_sat + exact_select; radius <= kExactFusedMaxRadius.
