@@ -83,6 +83,13 @@ const char* osbf_gpu_last_kernel(void);
  * default order.  No reference counterpart; results stay within fast mode's
  * tolerance whichever family runs. */
 osbf_status osbf_gpu_set_fast_kernel(const char* name);
+/* Diagnostics: force the kernel family of exact passes process-wide: "strip"
+ * (the fused strip walk, r <= 16), or the stencil of the whole-table path:
+ * "gwalk" (generic-radius walk, the default), "twalk" (templated walk,
+ * r <= 16), "stencil" (per-thread corner loads); NULL or "" = default.  A
+ * family that does not apply falls through to the next.  Every family is
+ * bit-identical to the reference.  No reference counterpart. */
+osbf_status osbf_gpu_set_exact_kernel(const char* name);
 /* Largest radius the fast mode serves with a fast kernel: radii up to 16 run
  * the templated kernels, larger ones the generic vertical-first walk (O(1)
  * state per thread in r) -- for whole planes up to r = 56, where the exact

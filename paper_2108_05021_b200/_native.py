@@ -35,6 +35,7 @@ SIGNATURES = [
     ("osbf_gpu_last_kernel", ctypes.c_char_p, []),
     ("osbf_gpu_fast_max_radius", _c_int, []),
     ("osbf_gpu_set_fast_kernel", _c_int, [ctypes.c_char_p]),
+    ("osbf_gpu_set_exact_kernel", _c_int, [ctypes.c_char_p]),
     ("osbf_gpu_device_available", _c_int, []),
     ("osbf_gpu_ctx_create", _c_int, [_c_int, ctypes.POINTER(_c_void_p)]),
     ("osbf_gpu_ctx_destroy", _c_int, [_c_void_p]),

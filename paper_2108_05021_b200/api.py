@@ -189,6 +189,13 @@ class Context:
         _check(N.lib().osbf_gpu_set_fast_kernel((name or "").encode()))
 
     @staticmethod
+    def set_exact_kernel(name: str | None) -> None:
+        """Diagnostics: force the exact-pass kernel family process-wide
+        (osbf_gpu_set_exact_kernel): "strip", "gwalk", "twalk", "stencil", or
+        None for the default (table path + generic walk).  All bit-identical."""
+        _check(N.lib().osbf_gpu_set_exact_kernel((name or "").encode()))
+
+    @staticmethod
     def fast_max_radius() -> int:
         """Largest radius with a fast kernel (osbf_gpu_fast_max_radius):
         16 templated radii, then the generic vertical-first walk."""

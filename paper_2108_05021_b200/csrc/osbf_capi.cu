@@ -80,6 +80,7 @@ struct GraphEntry {
     std::vector<uintptr_t> key;
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;  // kernels inside the graph (for the launch counter)
+    const char* kernel = "";  // kernel family of its last pass (osbf_gpu_last_kernel)
     int state = 0;          // 0 seen once (ran plain), 1 captured, -1 never capture
 };
 
@@ -183,18 +184,14 @@ int tb_env() {
     return k;
 }
 
-// OSBF_GPU_EXACT=table / strip: every exact pass on the whole-table path, or
-// on the fused strip walk whenever its radius allows (A/B runs and tests of
-// the path a launch would not pick by default).
-const char* exact_forced() {
-    static const char* v = [] {
-        const char* e = std::getenv("OSBF_GPU_EXACT");
-        return e ? e : "";
-    }();
-    return v;
+// The exact-pass family forced by osbf_gpu_set_exact_kernel or OSBF_GPU_EXACT
+// ("strip": the fused strip walk whenever its radius allows; "twalk" /
+// "gwalk" / "stencil": that stencil on the whole-table path) -- A/B runs and
+// tests of the kernels a launch would not pick by default.
+bool exact_strip_forced() {
+    const char* o = osbf_gpu::exact_kernel_override();
+    return o && std::strcmp(o, "strip") == 0;
 }
-bool exact_table_forced() { return std::strcmp(exact_forced(), "table") == 0; }
-bool exact_strip_forced() { return std::strcmp(exact_forced(), "strip") == 0; }
 
 // The fast-pass family forced by osbf_gpu_set_fast_kernel or OSBF_GPU_FAST.
 bool fast_family_forced(const char* name) {
@@ -236,8 +233,26 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
         }
         mode = OSBF_MODE_EXACT;
     }
-    if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius &&
-        !exact_table_forced() && (exact_strip_forced() || !osbf_gpu::exact_prefers_table(g))) {
+    // Exact mode runs the whole-table path (serial-order table build + the
+    // stencil walk: measured faster than the fused strip walk on every shape,
+    // profiles/r02_exact_paths.jsonl).  The fused strip walk (same bits, r <=
+    // 16) needs no table workspace: it serves when that workspace (two fp64
+    // planes) cannot be allocated, or when forced.
+    bool fused = false;
+    if (mode == OSBF_MODE_EXACT && dst && !means && !sel && r <= osbf_gpu::kExactFusedMaxRadius) {
+        fused = exact_strip_forced();
+        if (!fused) {
+            const size_t n = static_cast<size_t>(g.batch) * g.width * g.height;
+            const size_t tp = (static_cast<size_t>(g.width) + 2) & ~static_cast<size_t>(1);
+            const size_t ns = static_cast<size_t>(g.batch) * tp * (g.height + 1);
+            if (ctx->rowpfx.ensure(n * sizeof(double)) != cudaSuccess ||
+                ctx->sat.ensure((ns + 2) * sizeof(double)) != cudaSuccess) {
+                (void)cudaGetLastError();  // out of memory for the table: not an error yet
+                fused = true;
+            }
+        }
+    }
+    if (fused) {
         // fused exact path: row carries + strip kernel (same bits as below)
         OSBF_CUDA(ctx->rowpfx.ensure(osbf_gpu::exact_fused_carry_elems(g) * sizeof(double)),
                   "alloc carries");
@@ -250,12 +265,15 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
         const size_t tp = (static_cast<size_t>(g.width) + 2) & ~static_cast<size_t>(1);
         const size_t ns = static_cast<size_t>(g.batch) * tp * (g.height + 1);
         OSBF_CUDA(ctx->rowpfx.ensure(n * sizeof(double)), "alloc row prefix");
-        OSBF_CUDA(ctx->sat.ensure(ns * sizeof(double)), "alloc sat");
+        // + the table's own flag word behind it (cleared / raised by the
+        // build of every pass, read by the stencil)
+        OSBF_CUDA(ctx->sat.ensure((ns + 2) * sizeof(double)), "alloc sat");
+        unsigned* const tflag = reinterpret_cast<unsigned*>(ctx->sat.as<double>() + ns);
         OSBF_CUDA(osbf_gpu::exact_build_sat(src, g, ctx->rowpfx.as<double>(), ctx->sat.as<double>(),
-                                            s, ctx->lc, tp),
+                                            s, ctx->lc, tp, tflag),
                   "exact SAT");
         OSBF_CUDA(osbf_gpu::exact_select(src, g, r, ctx->sat.as<double>(), dst, dp, dpl, means, sel,
-                                         s, ctx->lc, tp),
+                                         s, ctx->lc, tp, tflag),
                   "exact select");
     } else {
         OSBF_CUDA(osbf_gpu::fast_step(src, g, r, dst, dp, dpl, means, sel, s, ctx->lc),
@@ -285,8 +303,21 @@ void note_kernel(const char* name) { g_last_kernel = name; }
 
 namespace {
 std::atomic<const char*> g_fast_override{nullptr};
+std::atomic<const char*> g_exact_override{nullptr};
+constexpr const char* kExactFamilies[] = {"strip", "twalk", "gwalk", "stencil"};
 }
 const char* fast_kernel_override() { return g_fast_override.load(std::memory_order_acquire); }
+const char* exact_kernel_override() {
+    if (const char* o = g_exact_override.load(std::memory_order_acquire)) return o;
+    static const char* env = []() -> const char* {
+        const char* e = std::getenv("OSBF_GPU_EXACT");
+        if (e)
+            for (const char* k : kExactFamilies)
+                if (std::strcmp(k, e) == 0) return k;
+        return nullptr;
+    }();
+    return env;
+}
 
 cudaError_t convert_to_f64(const PlaneView& in, const Geometry& g, double* out, size_t op,
                            size_t opl, cudaStream_t s, LaunchCounter& lc) {
@@ -393,6 +424,9 @@ osbf_status run_graphed(osbf_ctx* ctx, std::vector<uintptr_t> key, cudaStream_t 
         key.push_back(reinterpret_cast<uintptr_t>(p));
     for (size_t b : {ctx->ping.bytes, ctx->pong.bytes, ctx->rowpfx.bytes, ctx->sat.bytes})
         key.push_back(b);
+    // a forced kernel family is part of what a call launches
+    key.push_back(reinterpret_cast<uintptr_t>(osbf_gpu::fast_kernel_override()));
+    key.push_back(reinterpret_cast<uintptr_t>(osbf_gpu::exact_kernel_override()));
     auto it = std::find_if(ctx->graphs.begin(), ctx->graphs.end(),
                            [&](const GraphEntry& e) { return e.key == key; });
     if (it == ctx->graphs.end()) {
@@ -430,10 +464,12 @@ osbf_status run_graphed(osbf_ctx* ctx, std::vector<uintptr_t> key, cudaStream_t 
         }
         it->exec = exec;
         it->launches = captured;
+        it->kernel = g_last_kernel;
         it->state = 1;
     }
     OSBF_CUDA(cudaGraphLaunch(it->exec, s), "graph launch");
     ctx->lc.launches += it->launches;
+    g_last_kernel = it->kernel;
     return OSBF_OK;
 }
 
@@ -461,6 +497,19 @@ osbf_status osbf_gpu_set_fast_kernel(const char* name) {
             return OSBF_OK;
         }
     return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown fast kernel family '%s'", name);
+}
+
+osbf_status osbf_gpu_set_exact_kernel(const char* name) {
+    if (!name || !name[0]) {
+        osbf_gpu::g_exact_override.store(nullptr, std::memory_order_release);
+        return OSBF_OK;
+    }
+    for (const char* k : osbf_gpu::kExactFamilies)
+        if (std::strcmp(k, name) == 0) {
+            osbf_gpu::g_exact_override.store(k, std::memory_order_release);
+            return OSBF_OK;
+        }
+    return fail(OSBF_ERR_INVALID_ARGUMENT, "unknown exact kernel family '%s'", name);
 }
 
 int osbf_gpu_device_available(void) { return device_ok() ? 1 : 0; }

@@ -16,9 +16,11 @@
 // All fp64 arithmetic uses the _rn intrinsics so nothing is contracted.
 #include <atomic>
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "osbf_exact2_kernel.cuh"
+#include "osbf_exact_gwalk.cuh"
 #include "osbf_internal.cuh"
 
 namespace osbf_gpu {
@@ -30,8 +32,12 @@ constexpr int kChunk = 32;     // columns per transpose chunk
 template <typename T>
 __global__ void __launch_bounds__(kRowWarps * 32)
     exact_row_prefix(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
-                     double* __restrict__ rowpfx, int W, int H, long long total_rows) {
+                     double* __restrict__ rowpfx, int W, int H, long long total_rows,
+                     unsigned* __restrict__ reset_flag) {
     __shared__ double tile[kRowWarps][kChunk][kChunk + 1];
+    // the table flag of this pass starts clear (the column chains that may
+    // raise it run after this kernel, in stream order)
+    if (reset_flag && blockIdx.x == 0 && threadIdx.x == 0) *reset_flag = 0u;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const long long row0 = (static_cast<long long>(blockIdx.x) * kRowWarps + warp) * 32;
@@ -73,20 +79,22 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     }
 }
 
-// Sticky per-device flag: set (never cleared) by a column chain that produced
-// a table value outside the range where the 3-operation division is exact
-// (table_value_safe); the stencil then keeps the guarded division.  Set and
-// read in stream order (chain kernel, then stencil kernel).
+// Table flag: raised by a column chain that produced a table value outside
+// the range where the 3-operation division is exact (table_value_safe); the
+// stencil then keeps the guarded division.  Set and read in stream order
+// (chain kernel, then stencil kernel).  A caller that owns the table passes
+// its own flag word (cleared by the row-prefix kernel of every pass, so one
+// non-finite image does not slow later ones down); callers without one share
+// this sticky per-device word, which is never cleared.
 __device__ unsigned g_table_unsafe = 0u;
 
-__device__ __forceinline__ void flag_unsafe(bool unsafe) {
-    if (__any_sync(__activemask(), unsafe) && (threadIdx.x & 31) == 0)
-        atomicOr(&g_table_unsafe, 1u);
+__device__ __forceinline__ void flag_unsafe(unsigned* flag, bool unsafe) {
+    if (__any_sync(__activemask(), unsafe) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 // One thread per table column cx in [0, W] of each plane.
 __global__ void exact_col_chain(const double* __restrict__ rowpfx, double* __restrict__ sat,
-                                int W, int H, int B, long long tp) {
+                                int W, int H, int B, long long tp, unsigned* __restrict__ flag) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long cols = static_cast<long long>(W) + 1;
     if (t >= cols * B) return;
@@ -107,7 +115,7 @@ __global__ void exact_col_chain(const double* __restrict__ rowpfx, double* __res
         unsafe |= !table_value_safe(acc);
         C[static_cast<long long>(y + 1) * tp + cx] = acc;
     }
-    if (unsafe) atomicOr(&g_table_unsafe, 1u);
+    if (unsafe) atomicOr(flag, 1u);
 }
 
 // ---- deep-prefetch table builders (few planes) -------------------------------
@@ -163,11 +171,13 @@ __device__ __forceinline__ void mb_wait(uint64_t* bar, unsigned parity) {
 template <typename T>
 __global__ void __launch_bounds__(96)
     exact_row_prefix_deep(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
-                          double* __restrict__ rowpfx, int W, int H, long long total_rows) {
+                          double* __restrict__ rowpfx, int W, int H, long long total_rows,
+                          unsigned* __restrict__ reset_flag) {
     extern __shared__ double ring[];
     __shared__ uint64_t full[ROW_STAGES], done[ROW_STAGES], empty[ROW_STAGES];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long row0 = static_cast<long long>(blockIdx.x) * 32;
+    if (reset_flag && blockIdx.x == 0 && threadIdx.x == 0) *reset_flag = 0u;
     if (threadIdx.x == 0)
         for (int q = 0; q < ROW_STAGES; ++q) {
             mb_init(&full[q], 32);
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(96)
 // only load / add / store per element.
 __global__ void __launch_bounds__(96)
     exact_col_chain_deep(const double* __restrict__ rowpfx, double* __restrict__ sat, int W,
-                         int H, int B, long long tp) {
+                         int H, int B, long long tp, unsigned* __restrict__ flag) {
     extern __shared__ double cring[];
     __shared__ uint64_t full[COL_STAGES], done[COL_STAGES], empty[COL_STAGES];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(96)
                 }
             }
         }
-        flag_unsafe(unsafe);
+        flag_unsafe(flag, unsafe);
     }
 }
 
@@ -444,6 +454,16 @@ __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_p
     if (sel) sel[pix] = static_cast<uint8_t>(best_id);
 }
 
+// The shared sticky flag word (callers that pass no flag of their own).
+unsigned* table_flag_address() {
+    static unsigned* flag = [] {
+        void* p = nullptr;
+        return cudaGetSymbolAddress(&p, g_table_unsafe) == cudaSuccess ? static_cast<unsigned*>(p)
+                                                                       : nullptr;
+    }();
+    return flag;
+}
+
 constexpr int kStencilRows = 4;  // rows per thread (block: 32 x 8 threads, 32 x 32 pixels)
 
 template <typename T, int RT>
@@ -451,11 +471,12 @@ __global__ void __launch_bounds__(256)
     exact_stencil(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
                   const double* __restrict__ sat, double* __restrict__ out, size_t out_pitch,
                   size_t out_plane, double* __restrict__ means, uint8_t* __restrict__ sel, int W,
-                  int H, int r_rt, double yq, double yh, long long cols) {
+                  int H, int r_rt, double yq, double yh, long long cols,
+                  const unsigned* __restrict__ flag) {
     const int r = RT > 0 ? RT : r_rt;
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const int b = blockIdx.z;
-    const bool safe = *reinterpret_cast<volatile unsigned*>(&g_table_unsafe) == 0u;
+    const bool safe = *flag == 0u;
     const double* C = sat + static_cast<long long>(b) * cols * (H + 1);
     const int ic = static_cast<int>(cols);
     const int ro1 = r * ic, ro2 = (r + 1) * ic, ro3 = (2 * r + 1) * ic;
@@ -470,18 +491,18 @@ __global__ void __launch_bounds__(256)
 template <typename T, int RT>
 void launch_stencil_rt(dim3 grid, cudaStream_t s, const T* in, size_t ip, size_t ipl,
                        const double* sat, double* out, size_t op, size_t opl, int W, int H, int r,
-                       double yq, double yh, long long tp) {
+                       double yq, double yh, long long tp, const unsigned* flag) {
     exact_stencil<T, RT><<<grid, 256, 0, s>>>(in, ip, ipl, sat, out, op, opl, nullptr, nullptr, W,
-                                              H, r, yq, yh, tp);
+                                              H, r, yq, yh, tp, flag);
 }
 template <typename T, int... Rs>
 bool launch_stencil_fixed(std::integer_sequence<int, Rs...>, dim3 grid, cudaStream_t s,
                           const T* in, size_t ip, size_t ipl, const double* sat, double* out,
                           size_t op, size_t opl, int W, int H, int r, double yq, double yh,
-                          long long tp) {
+                          long long tp, const unsigned* flag) {
     bool hit = false;
     ((r == Rs + 1 ? (launch_stencil_rt<T, Rs + 1>(grid, s, in, ip, ipl, sat, out, op, opl, W, H,
-                                                  r, yq, yh, tp),
+                                                  r, yq, yh, tp, flag),
                      hit = true)
                   : false),
      ...);
@@ -490,19 +511,20 @@ bool launch_stencil_fixed(std::integer_sequence<int, Rs...>, dim3 grid, cudaStre
 
 template <typename T>
 cudaError_t launch_row_prefix(const PlaneView& in, const Geometry& g, double* rowpfx,
-                              cudaStream_t s) {
+                              cudaStream_t s, unsigned* reset_flag) {
     const long long rows = static_cast<long long>(g.batch) * g.height;
     const long long warps = (rows + 31) / 32;
     const unsigned blocks = static_cast<unsigned>((warps + kRowWarps - 1) / kRowWarps);
     exact_row_prefix<T><<<blocks, kRowWarps * 32, 0, s>>>(
-        static_cast<const T*>(in.base), in.pitch, in.plane, rowpfx, g.width, g.height, rows);
+        static_cast<const T*>(in.base), in.pitch, in.plane, rowpfx, g.width, g.height, rows,
+        reset_flag);
     return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const double* sat,
                            double* out, size_t op, size_t opl, double* means, uint8_t* sel,
-                           cudaStream_t s, long long tp) {
+                           cudaStream_t s, long long tp, const unsigned* flag) {
     dim3 grid((g.width + 31) / 32, (g.height + 8 * kStencilRows - 1) / (8 * kStencilRows),
               g.batch);
     // interior reciprocals RN(1/n) (IEEE on the host, the same value)
@@ -514,12 +536,12 @@ cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const 
         if (!means && !sel && out &&
             launch_stencil_fixed<T>(std::make_integer_sequence<int, 16>{}, grid, s,
                                     static_cast<const T*>(in.base), in.pitch, in.plane, sat, out,
-                                    op, opl, g.width, g.height, r, yq, yh, tp))
+                                    op, opl, g.width, g.height, r, yq, yh, tp, flag))
             return cudaGetLastError();
     }
     exact_stencil<T, 0><<<grid, 256, 0, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane,
                                              sat, out, op, opl, means, sel, g.width, g.height, r,
-                                             yq, yh, tp);
+                                             yq, yh, tp, flag);
     return cudaGetLastError();
 }
 
@@ -529,29 +551,43 @@ cudaError_t launch_stencil(const PlaneView& in, const Geometry& g, int r, const 
 // prefetch builders; same chains, same table.
 template <typename T>
 cudaError_t launch_row_prefix_deep(const PlaneView& in, const Geometry& g, double* rowpfx,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, unsigned* reset_flag) {
     static std::atomic<unsigned long long> done{0};
     if (cudaError_t e = ensure_smem(exact_row_prefix_deep<T>, ROW2_SMEM, done)) return e;
     const long long rows = static_cast<long long>(g.batch) * g.height;
     exact_row_prefix_deep<T><<<static_cast<unsigned>((rows + 31) / 32), 96, ROW2_SMEM, s>>>(
-        static_cast<const T*>(in.base), in.pitch, in.plane, rowpfx, g.width, g.height, rows);
+        static_cast<const T*>(in.base), in.pitch, in.plane, rowpfx, g.width, g.height, rows,
+        reset_flag);
     return cudaGetLastError();
 }
 
 bool table_deep(const Geometry& g) {
+    static const int forced = [] {  // OSBF_GPU_TABLE_DEEP=0/1: A/B runs
+        const char* e = std::getenv("OSBF_GPU_TABLE_DEEP");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    if (forced >= 0) return forced != 0;
+    // measured (r02_exact_paths.jsonl): 2048 chain warps (64 x 1024^2) 1.12 vs
+    // 1.38 ms per pass, 1024 warps (16 x 2048^2) 1.12 vs 1.95; 8192 warps
+    // (256 x 1024^2) 4.33 vs 4.14
     const long long warps = (static_cast<long long>(g.batch) * g.height + 31) / 32;
-    return warps <= 4 * 148;
+    return warps <= 4096;
 }
 
 cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
-                            cudaStream_t s, LaunchCounter& lc, size_t tpitch) {
+                            cudaStream_t s, LaunchCounter& lc, size_t tpitch, unsigned* table_flag) {
     const long long tp = tpitch ? static_cast<long long>(tpitch) : g.width + 1LL;
     cudaError_t e;
+    // the caller's own flag word is cleared by the row-prefix kernel; the
+    // shared word stays sticky
+    unsigned* const reset = table_flag;
+    unsigned* const flag = table_flag ? table_flag : table_flag_address();
+    if (!flag) return cudaErrorInvalidDevicePointer;
     if (table_deep(g)) {
         switch (in.dtype) {
-            case OSBF_U8: e = launch_row_prefix_deep<uint8_t>(in, g, rowpfx, s); break;
-            case OSBF_F32: e = launch_row_prefix_deep<float>(in, g, rowpfx, s); break;
-            default: e = launch_row_prefix_deep<double>(in, g, rowpfx, s); break;
+            case OSBF_U8: e = launch_row_prefix_deep<uint8_t>(in, g, rowpfx, s, reset); break;
+            case OSBF_F32: e = launch_row_prefix_deep<float>(in, g, rowpfx, s, reset); break;
+            default: e = launch_row_prefix_deep<double>(in, g, rowpfx, s, reset); break;
         }
         ++lc.launches;
         if (e != cudaSuccess) return e;
@@ -559,20 +595,20 @@ cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowp
         if ((e = ensure_smem(exact_col_chain_deep, COL2_SMEM, done)) != cudaSuccess) return e;
         const long long wpp = (static_cast<long long>(g.width) + 1 + 31) / 32;
         exact_col_chain_deep<<<static_cast<unsigned>(wpp * g.batch), 96, COL2_SMEM, s>>>(
-            rowpfx, sat, g.width, g.height, g.batch, tp);
+            rowpfx, sat, g.width, g.height, g.batch, tp, flag);
         ++lc.launches;
         return cudaGetLastError();
     }
     switch (in.dtype) {
-        case OSBF_U8: e = launch_row_prefix<uint8_t>(in, g, rowpfx, s); break;
-        case OSBF_F32: e = launch_row_prefix<float>(in, g, rowpfx, s); break;
-        default: e = launch_row_prefix<double>(in, g, rowpfx, s); break;
+        case OSBF_U8: e = launch_row_prefix<uint8_t>(in, g, rowpfx, s, reset); break;
+        case OSBF_F32: e = launch_row_prefix<float>(in, g, rowpfx, s, reset); break;
+        default: e = launch_row_prefix<double>(in, g, rowpfx, s, reset); break;
     }
     ++lc.launches;
     if (e != cudaSuccess) return e;
     const long long threads = (static_cast<long long>(g.width) + 1) * g.batch;
     exact_col_chain<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(
-        rowpfx, sat, g.width, g.height, g.batch, tp);
+        rowpfx, sat, g.width, g.height, g.batch, tp, flag);
     ++lc.launches;
     return cudaGetLastError();
 }
@@ -590,48 +626,54 @@ constexpr TwalkFn kTwalk[kExactFusedMaxRadius + 1] = {
     exact_twalk_launch<16>,
 };
 
-// OSBF_GPU_TWALK=0: keep the per-thread corner-load stencil (A/B runs, tests).
-bool twalk_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("OSBF_GPU_TWALK");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+// Stencil family of a table-path pass: the generic walk (any r <= 62), then
+// the templated walk (r <= 16), then the per-thread stencil; an override
+// (exact_kernel_override) starts further down the list.
+int stencil_family_start() {
+    const char* o = exact_kernel_override();
+    if (o && std::strcmp(o, "twalk") == 0) return 1;
+    if (o && std::strcmp(o, "stencil") == 0) return 2;
+    return 0;
 }
 }  // namespace
 
 cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
                          double* out, size_t out_pitch, size_t out_plane, double* means,
-                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch) {
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch,
+                         const unsigned* table_flag) {
     ++lc.launches;
     const long long tp = tpitch ? static_cast<long long>(tpitch) : g.width + 1LL;
-    if (out && !means && !sel && radius <= kExactFusedMaxRadius && twalk_enabled()) {
-        static unsigned* flag = [] {
-            void* p = nullptr;
-            return cudaGetSymbolAddress(&p, g_table_unsafe) == cudaSuccess
-                       ? static_cast<unsigned*>(p)
-                       : nullptr;
-        }();
-        if (flag) {
-            const cudaError_t e = kTwalk[radius](in, g, sat, static_cast<size_t>(tp), out,
+    const unsigned* const flag = table_flag ? table_flag : table_flag_address();
+    if (!flag) return cudaErrorInvalidDevicePointer;
+    const int start = stencil_family_start();
+    if (out && !means && !sel && start <= 0) {
+        // any radius up to 62: three TMA streams of table rows per CTA
+        const cudaError_t e = exact_gwalk_launch(in, g, radius, sat, static_cast<size_t>(tp), out,
                                                  out_pitch, out_plane, flag, s);
-            if (e != cudaErrorNotSupported) {
-                note_kernel("exact_row_prefix+exact_col_chain+exact_twalk");
-                return e;
-            }
+        if (e != cudaErrorNotSupported) {
+            note_kernel("exact_row_prefix+exact_col_chain+exact_gwalk");
+            return e;
+        }
+    }
+    if (out && !means && !sel && radius <= kExactFusedMaxRadius && start <= 1) {
+        const cudaError_t e = kTwalk[radius](in, g, sat, static_cast<size_t>(tp), out, out_pitch,
+                                             out_plane, flag, s);
+        if (e != cudaErrorNotSupported) {
+            note_kernel("exact_row_prefix+exact_col_chain+exact_twalk");
+            return e;
         }
     }
     note_kernel("exact_row_prefix+exact_col_chain+exact_select");
     switch (in.dtype) {
         case OSBF_U8:
             return launch_stencil<uint8_t>(in, g, radius, sat, out, out_pitch, out_plane, means,
-                                           sel, s, tp);
+                                           sel, s, tp, flag);
         case OSBF_F32:
             return launch_stencil<float>(in, g, radius, sat, out, out_pitch, out_plane, means, sel,
-                                         s, tp);
+                                         s, tp, flag);
         default:
             return launch_stencil<double>(in, g, radius, sat, out, out_pitch, out_plane, means,
-                                          sel, s, tp);
+                                          sel, s, tp, flag);
     }
 }
 
@@ -692,14 +734,6 @@ int exact_band_height(const Geometry& g) {
     int bh = static_cast<int>((g.height + nb - 1) / nb);
     bh = (bh + ex2::BR - 1) / ex2::BR * ex2::BR;
     return bh < 128 ? 128 : bh;
-}
-
-bool exact_prefers_table(const Geometry& g) {
-    // measured (4096^2: 0.56 vs 0.64-1.00 ms per pass over r = 1..16;
-    // 1920x1080: 0.13 vs 0.17-0.23 ms; 64 x 1024^2 stays on the strip walk,
-    // 1.15 vs 1.73 ms)
-    const long long strips = (static_cast<long long>(g.width) + ex2::TW - 1) / ex2::TW;
-    return strips * g.batch < 2 * 148;
 }
 
 size_t exact_fused_carry_elems(const Geometry& g) {

@@ -70,6 +70,11 @@ void note_kernel(const char* name);
 // diagnostics / A-B tests); null = none.
 const char* fast_kernel_override();
 
+// Process-wide override of the exact-pass kernel family
+// (osbf_gpu_set_exact_kernel / OSBF_GPU_EXACT: "strip", "twalk", "gwalk",
+// "stencil"); null = none.  Every family is bit-identical.
+const char* exact_kernel_override();
+
 // Launch statistics (kernels issued) for instrumentation.
 struct LaunchCounter {
     uint64_t launches = 0;
@@ -81,15 +86,20 @@ struct LaunchCounter {
 //   sat   : fp64 [batch][height+1][width+1]
 //   tpitch: table row pitch in doubles (0 = width+1; the osbf pass path uses
 //           an even pitch so the stencil walk can stage table rows with TMA)
+//   table_flag: the caller's "table leaves the exact division's range" word
+//           (device memory, cleared and set by the build, read by
+//           exact_select); null = a sticky per-device word shared by all callers
 cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowpfx, double* sat,
-                            cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0);
+                            cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0,
+                            unsigned* table_flag = nullptr);
 // One exact OSBF pass reading `in` and the SAT built from it.
 //   out   : fp64 (nullable), out_pitch / out_plane in elements
 //   means : fp64 [batch][height][width][8] (nullable)
 //   sel   : uint8 [batch][height][width] (nullable)
 cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, const double* sat,
                          double* out, size_t out_pitch, size_t out_plane, double* means,
-                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0);
+                         uint8_t* sel, cudaStream_t s, LaunchCounter& lc, size_t tpitch = 0,
+                         const unsigned* table_flag = nullptr);
 
 // Table-path stencil as a TMA-staged column walk (osbf_exact_twalk.cuh,
 // instantiated per radius in osbf_exact2_rNN.cu); cudaErrorNotSupported
@@ -103,10 +113,6 @@ cudaError_t exact_twalk_launch(const PlaneView& in, const Geometry& g, const dou
 // Bit-identical to exact_build_sat + exact_select; radius <= kExactFusedMaxRadius.
 constexpr int kExactFusedMaxRadius = 16;
 size_t exact_fused_carry_elems(const Geometry& g);
-// Few strips x planes (one 4096^2 plane: 128): the fused strip walk cannot
-// fill the device, and the whole-table path (deep-prefetch serial chains +
-// a fully parallel stencil) is faster -- same table, same bits.
-bool exact_prefers_table(const Geometry& g);
 cudaError_t exact_fused_step(const PlaneView& in, const Geometry& g, int radius, double* carries,
                              double* out, size_t out_pitch, size_t out_plane, cudaStream_t s,
                              LaunchCounter& lc);

@@ -63,10 +63,16 @@ def test_launch_counter_counts_kernels(ctx):
     # (row prefixes, column chains, stencil)
     assert ctx.launches - before == 9 and "exact_col_chain" in ctx.last_kernel
     xb = torch.rand((300, 64, 64), dtype=torch.float64, device="cuda")
-    before = ctx.launches
-    ctx.iterate(xb, 2, 3, mode="exact")
-    # enough strips x planes for the fused walk: 2 kernels per pass (row carries + strip)
-    assert ctx.launches - before == 6 and "exact_strip" in ctx.last_kernel
+    import paper_2108_05021_b200 as ob
+
+    ob.Context.set_exact_kernel("strip")
+    try:
+        before = ctx.launches
+        ctx.iterate(xb, 2, 3, mode="exact")
+        # the fused strip walk: 2 kernels per pass (row carries + strip)
+        assert ctx.launches - before == 6 and "exact_strip" in ctx.last_kernel
+    finally:
+        ob.Context.set_exact_kernel(None)
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="fast")
     assert ctx.launches - before == 3

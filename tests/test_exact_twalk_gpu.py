@@ -3,15 +3,25 @@
 radius the walk is compiled for, every input dtype, clipped borders, row
 blocks, several planes, and non-finite samples (guarded fallback).
 
-A lone plane or a few planes take the table path (exact_prefers_table);
-widths whose rows are not 16-byte multiples fall back to the per-thread
-stencil, so both are covered here."""
+The templated walk is a selectable family (the default stencil is the
+generic-radius walk, osbf_exact_gwalk.cuh), forced here; widths whose rows
+are not 16-byte multiples fall back to the per-thread stencil, so both are
+covered."""
 import numpy as np
 import pytest
 
 from conftest import bits
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def twalk_family():
+    import paper_2108_05021_b200 as ob
+
+    ob.Context.set_exact_kernel("twalk")
+    yield
+    ob.Context.set_exact_kernel(None)
 
 
 def dev(a):

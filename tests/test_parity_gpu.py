@@ -86,10 +86,19 @@ def test_exact_row_bands_bit_exact(ctx, oracle_lib, shape, r, scale):
     """Tall planes with few 32-column strips run the exact strip kernel in
     row bands that start from stored table rows; must stay bit-exact,
     including values whose window divisions take the guarded path."""
+    import paper_2108_05021_b200 as ob
+
     rng = np.random.default_rng(sum(shape) + r)
     p = rng.random(shape) * scale
-    got = ctx.iterate(torch_dev(p), r, 2, mode="exact").cpu().numpy()
     want = np.stack([oracle_lib.osbf(c, r, 2, threads=8) for c in p])
+    ob.Context.set_exact_kernel("strip")  # (the default is the whole-table path)
+    try:
+        got = ctx.iterate(torch_dev(p), r, 2, mode="exact").cpu().numpy()
+        assert "exact_strip" in ctx.last_kernel
+    finally:
+        ob.Context.set_exact_kernel(None)
+    assert np.array_equal(bits(got), bits(want))
+    got = ctx.iterate(torch_dev(p), r, 2, mode="exact").cpu().numpy()
     assert np.array_equal(bits(got), bits(want))
 
 
