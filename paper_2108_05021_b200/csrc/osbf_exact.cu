@@ -340,6 +340,290 @@ __global__ void __launch_bounds__(96)
     }
 }
 
+// ---- strip table builder ------------------------------------------------------
+// The table straight from the input, without the row-prefix plane: the row
+// carries R(16s-1, y) come from exact_row_carries (osbf_exact2_kernel.cuh, K1
+// of the fused path), then one CTA per 32-column strip of a plane walks down
+// it in 32 x 32 tiles as a four-warp pipeline on mbarriers over a ring of
+// padded 32 x 33 transpose tiles:
+//   warp 0 loads tile t of U (lanes = columns, coalesced),
+//   warp 1 continues the 32 row chains from their carries, in place
+//          (lanes = rows; row += src[x], integral.hpp:25),
+//   warp 2 continues the 32 column chains down the tile, in place
+//          (lanes = columns; above[x+1] + row, integral.hpp:26),
+//   warp 3 stores the table rows (coalesced) and flags unsafe values.
+// Same serial adds in the same order as exact_row_prefix + exact_col_chain:
+// the table is bit-identical, and the row-prefix plane's write and re-read
+// (half the build's HBM traffic) is gone.
+constexpr int TS_STAGES = 6;        // many CTAs per SM
+constexpr int TS_STAGES_DEEP = 16;  // about one CTA per SM: hide the full HBM latency
+constexpr int TS_LOADERS = 4;  // loader warps (8 tile rows each)
+constexpr int TS_STORERS = 2;  // storer warps (16 tile rows each)
+constexpr int TS_THREADS = 32 * (TS_LOADERS + 2 + TS_STORERS);
+constexpr int TS_TILE = 32 * 33 + 32;  // padded transpose tile + the 32 row carries of the tile
+
+// One arrival per warp: the lanes' shared-memory accesses are ordered before
+// it by the warp barrier (32 per-lane arrivals on one mbarrier word serialise).
+__device__ __forceinline__ void mb_arrive_warp(uint64_t* bar, int lane) {
+    __syncwarp();
+    if (lane == 0) mb_arrive(bar);
+}
+
+// Rows rr0 .. rr0 + 7 of a 32 x 32 tile into a padded transpose tile
+// (element (column lane, row rr) at tile[lane * 33 + rr]); src points at this
+// lane's column in tile row 0, rows_left = valid rows from there, col_ok =
+// the lane's column exists.  fp64 input goes through cp.async (arrival on
+// `bar` when the copies land), narrower types through registers.
+template <typename T>
+__device__ __forceinline__ void load_tile_rows(double* tile, const T* src, size_t pitch, int rr0,
+                                               int rows_left, bool col_ok, int lane,
+                                               uint64_t* bar) {
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int j = 0; j < 32 / TS_LOADERS; ++j) {
+            const int rr = rr0 + j;
+            const bool ok = col_ok && rr < rows_left;
+            cpa8(tile + lane * 33 + rr,
+                 reinterpret_cast<const double*>(src) + (ok ? static_cast<size_t>(rr) * pitch : 0),
+                 ok);
+        }
+        mb_arrive_cpasync(bar);
+    } else {
+        T v[32 / TS_LOADERS];
+#pragma unroll
+        for (int j = 0; j < 32 / TS_LOADERS; ++j) {
+            const int rr = rr0 + j;
+            const bool ok = col_ok && rr < rows_left;
+            v[j] = ok ? src[static_cast<size_t>(rr) * pitch] : T(0);
+        }
+#pragma unroll
+        for (int j = 0; j < 32 / TS_LOADERS; ++j) tile[lane * 33 + rr0 + j] = to_f64(v[j]);
+        mb_arrive(bar);
+    }
+}
+
+constexpr size_t ts_smem(int stages) { return sizeof(double) * static_cast<size_t>(stages) * TS_TILE; }
+
+// A strip is the 32 TABLE columns cx = 32 j .. 32 j + 31 (so a bulk store of
+// its tiles starts on a 16-byte boundary); table column cx holds the running
+// row sums R(cx - 1, y): the strip's first column is the stored carry
+// R(32 j - 1, y) itself (0 for j = 0: the table's zero column), the others
+// continue it with U(32 j .. 32 j + 30).
+// (A variant whose column-chain warp wrote dense tiles and stored them with
+// cp.async.bulk.tensor measured slower, 338 vs 216 us on 64 x 1024^2: the
+// extra shared stores and the issue of the bulk store serialise on the one
+// chain warp; two storer warps write the rows instead.)
+template <typename T, int NST>
+__global__ void __launch_bounds__(TS_THREADS)
+    exact_table_strip(const T* __restrict__ in, size_t in_pitch, size_t in_plane,
+                      const double* __restrict__ carries, int nsc, double* __restrict__ sat,
+                      long long tp, int W, int H, unsigned* __restrict__ flag) {
+    extern __shared__ double tring[];
+    __shared__ uint64_t full[NST], rdone[NST], cdone[NST], empty[NST];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.y;
+    const int x0 = blockIdx.x * 32;
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NST; ++q) {
+            mb_init(&full[q], 32 * TS_LOADERS);
+            mb_init(&rdone[q], 1);
+            mb_init(&cdone[q], 1);
+            mb_init(&empty[q], TS_STORERS);
+        }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    const int ntiles = (H + 31) / 32;
+    const int x = x0 + lane;  // table column of this lane (column chains, stores)
+    const int ux = x - 1;     // input column feeding it (lane 0: the carry, no input)
+    const bool u_ok = ux >= 0 && ux < W && lane > 0;
+    double* C = sat + static_cast<long long>(b) * tp * (H + 1);
+    if (warp < TS_LOADERS) {
+        const T* src = in + static_cast<size_t>(b) * in_plane + (u_ok ? ux : 0);
+        // loader 0 also brings the tile's row carries R(x0 - 1, y), lane = row
+        const double* crow = carries + static_cast<size_t>(b) * H * nsc + x0 / 16;
+        for (int t = 0; t < ntiles; ++t) {
+            const int q = t % NST;
+            if (t >= NST) mb_wait(&empty[q], ((t / NST) - 1) & 1);
+            double* tile = tring + q * TS_TILE;
+            if (warp == 0) {
+                const int y = t * 32 + lane;
+                const bool ok = y < H;
+                if constexpr (sizeof(T) == 8)
+                    cpa8(tile + 32 * 33 + lane, crow + (ok ? static_cast<size_t>(y) * nsc : 0), ok);
+                else
+                    tile[32 * 33 + lane] = ok ? crow[static_cast<size_t>(y) * nsc] : 0.0;
+            }
+            load_tile_rows<T>(tile, src + static_cast<size_t>(t) * 32 * in_pitch, in_pitch,
+                              warp * (32 / TS_LOADERS), H - t * 32, u_ok, lane, &full[q]);
+        }
+    } else if (warp == TS_LOADERS) {
+        // lane = row of the tile: column 0 is the carry R(x0 - 1, y), then the chain
+        const int n = min(32, W + 1 - x0);  // table columns of this strip
+        for (int t = 0; t < ntiles; ++t) {
+            const int q = t % NST;
+            mb_wait(&full[q], (t / NST) & 1);
+            double* tile = tring + q * TS_TILE;
+            double acc = tile[32 * 33 + lane];
+            double v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = tile[k * 33 + lane];
+            tile[lane] = acc;
+            if (n == 32) {  // nothing but the adds on the dependent chain
+#pragma unroll
+                for (int k = 1; k < 32; ++k) {
+                    acc = __dadd_rn(acc, v[k]);
+                    tile[k * 33 + lane] = acc;
+                }
+            } else {  // last, partial strip
+#pragma unroll
+                for (int k = 1; k < 32; ++k) {
+                    if (k < n) {
+                        acc = __dadd_rn(acc, v[k]);
+                        tile[k * 33 + lane] = acc;
+                    }
+                }
+            }
+            mb_arrive_warp(&rdone[q], lane);
+        }
+    } else if (warp == TS_LOADERS + 1) {
+        double acc = 0.0;  // lane = table column x: C(x, y) so far
+        // zero border row 0 of the table over this strip's columns
+        if (x <= W) C[x] = 0.0;
+        for (int t = 0; t < ntiles; ++t) {
+            const int q = t % NST;
+            mb_wait(&rdone[q], (t / NST) & 1);
+            double* tile = tring + q * TS_TILE;
+            double v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = tile[lane * 33 + k];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                acc = __dadd_rn(acc, v[k]);
+                tile[lane * 33 + k] = acc;
+            }
+            mb_arrive_warp(&cdone[q], lane);
+        }
+    } else {
+        constexpr int RPS = 32 / TS_STORERS;  // tile rows per storer warp
+        const int k0 = (warp - TS_LOADERS - 2) * RPS;
+        bool unsafe = false;
+        for (int t = 0; t < ntiles; ++t) {
+            const int q = t % NST;
+            mb_wait(&cdone[q], (t / NST) & 1);
+            const double* tile = tring + q * TS_TILE;
+            double v[RPS];
+#pragma unroll
+            for (int k = 0; k < RPS; ++k) v[k] = tile[lane * 33 + k0 + k];
+            mb_arrive_warp(&empty[q], lane);
+            const int nk = min(RPS, H - t * 32 - k0);  // may be <= 0
+            double* cp = C + static_cast<long long>(t * 32 + k0 + 1) * tp + x;
+            if (x <= W) {
+#pragma unroll
+                for (int k = 0; k < RPS; ++k) {
+                    if (k < nk) {
+                        unsafe |= !table_value_safe(v[k]);
+                        cp[static_cast<long long>(k) * tp] = v[k];
+                    }
+                }
+            }
+        }
+        flag_unsafe(flag, unsafe);
+    }
+}
+
+// The row carries R(16 s - 1, y) for few rows (about one chain warp per SM
+// or fewer): CTA per 32 rows as loader warps + one chain warp over a ring of
+// 32 x 32 chunks, so the serial chain (row += src[x], integral.hpp:25) is not
+// slowed by the copy instructions.  Same values as ex2::exact_row_carries.
+constexpr int RC_STAGES = 16;
+constexpr size_t RC_SMEM = sizeof(double) * RC_STAGES * 32 * 33;
+
+template <typename T>
+__global__ void __launch_bounds__(32 * (TS_LOADERS + 1))
+    exact_row_carries_pipe(const T* __restrict__ in, size_t pitch, size_t plane,
+                           double* __restrict__ carries, int W, int H, long long rows, int nsc) {
+    extern __shared__ double cring[];
+    __shared__ uint64_t full[RC_STAGES], empty[RC_STAGES];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long row0 = static_cast<long long>(blockIdx.x) * 32;
+    if (threadIdx.x == 0)
+        for (int q = 0; q < RC_STAGES; ++q) {
+            mb_init(&full[q], 32 * TS_LOADERS);
+            mb_init(&empty[q], 1);
+        }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    const int nchunks = (W + 31) / 32;
+    if (warp < TS_LOADERS) {
+        // element offsets of this warp's 8 rows (rows may straddle planes)
+        constexpr int RPL = 32 / TS_LOADERS;
+        long long base[RPL];
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+            const long long g = row0 + warp * RPL + j;
+            base[j] = -1;
+            if (g < rows) {
+                const long long b = g / H, y = g - b * H;
+                base[j] = b * static_cast<long long>(plane) + y * static_cast<long long>(pitch);
+            }
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const int q = c % RC_STAGES;
+            if (c >= RC_STAGES) mb_wait(&empty[q], ((c / RC_STAGES) - 1) & 1);
+            double* t = cring + q * 32 * 33;
+            const int x = 32 * c + lane;
+            if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                for (int j = 0; j < RPL; ++j) {
+                    const bool ok = base[j] >= 0 && x < W;
+                    cpa8(t + lane * 33 + warp * RPL + j,
+                         reinterpret_cast<const double*>(in) + (ok ? base[j] + x : 0), ok);
+                }
+                mb_arrive_cpasync(&full[q]);
+            } else {
+                T v[RPL];
+#pragma unroll
+                for (int j = 0; j < RPL; ++j)
+                    v[j] = (base[j] >= 0 && x < W) ? in[base[j] + x] : T(0);
+#pragma unroll
+                for (int j = 0; j < RPL; ++j) t[lane * 33 + warp * RPL + j] = to_f64(v[j]);
+                mb_arrive(&full[q]);
+            }
+        }
+    } else {
+        const long long g = row0 + lane;
+        double* crow = carries + (g < rows ? g : 0) * nsc;
+        if (g < rows) crow[0] = 0.0;
+        double acc = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int q = c % RC_STAGES;
+            mb_wait(&full[q], (c / RC_STAGES) & 1);
+            const double* t = cring + q * 32 * 33;
+            double v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = t[k * 33 + lane];
+            mb_arrive_warp(&empty[q], lane);
+            const int n = min(32, W - 32 * c);
+            if (n == 32) {  // nothing but the adds on the dependent chain
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    acc = __dadd_rn(acc, v[k]);
+                    if ((k + 1) % ex2::SW == 0 && g < rows) crow[(32 * c + k + 1) / ex2::SW] = acc;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    if (k < n) {
+                        acc = __dadd_rn(acc, v[k]);
+                        if ((k + 1) % ex2::SW == 0 && g < rows)
+                            crow[(32 * c + k + 1) / ex2::SW] = acc;
+                    }
+                }
+            }
+        }
+    }
+}
+
 // C / cols: the table of plane b (or a shared-memory copy of the part this
 // pixel reads: C then points at the copy's virtual origin, cols is its pitch).
 // RT > 0: the radius as a compile-time constant (corner offsets become
@@ -561,6 +845,24 @@ cudaError_t launch_row_prefix_deep(const PlaneView& in, const Geometry& g, doubl
     return cudaGetLastError();
 }
 
+// Table build family: the strip builder (row carries + exact_table_strip) or
+// the two chain kernels (OSBF_GPU_TABLE=chains: A/B runs, tests).
+bool table_chains_forced() {
+    static const bool on = [] {
+        const char* e = std::getenv("OSBF_GPU_TABLE");
+        return e && std::strcmp(e, "chains") == 0;
+    }();
+    return on;
+}
+cudaError_t build_sat_strips(const PlaneView& in, const Geometry& g, double* carries, double* sat,
+                             long long tp, unsigned* flag, unsigned* reset, cudaStream_t s,
+                             LaunchCounter& lc);
+
+bool table_deep(const Geometry& g);
+bool table_uses_strips(const PlaneView& in, const Geometry& g) {
+    return !table_chains_forced() && !(in.dtype == OSBF_F32 && !table_deep(g));
+}
+
 bool table_deep(const Geometry& g) {
     static const int forced = [] {  // OSBF_GPU_TABLE_DEEP=0/1: A/B runs
         const char* e = std::getenv("OSBF_GPU_TABLE_DEEP");
@@ -583,6 +885,10 @@ cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowp
     unsigned* const reset = table_flag;
     unsigned* const flag = table_flag ? table_flag : table_flag_address();
     if (!flag) return cudaErrorInvalidDevicePointer;
+    // float32 input (a first pass) with many rows: the strip builder's
+    // register-staged loads lose to the plain chain kernels (256 x 1024^2:
+    // 4.5-5.5 vs 3.7 ms); every other case builds by strips
+    if (table_uses_strips(in, g)) return build_sat_strips(in, g, rowpfx, sat, tp, flag, reset, s, lc);
     if (table_deep(g)) {
         switch (in.dtype) {
             case OSBF_U8: e = launch_row_prefix_deep<uint8_t>(in, g, rowpfx, s, reset); break;
@@ -645,13 +951,16 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
     const long long tp = tpitch ? static_cast<long long>(tpitch) : g.width + 1LL;
     const unsigned* const flag = table_flag ? table_flag : table_flag_address();
     if (!flag) return cudaErrorInvalidDevicePointer;
+    // label: the table build of this pass + the stencil family
+    const bool chains = !table_uses_strips(in, g);
     const int start = stencil_family_start();
     if (out && !means && !sel && start <= 0) {
         // any radius up to 62: three TMA streams of table rows per CTA
         const cudaError_t e = exact_gwalk_launch(in, g, radius, sat, static_cast<size_t>(tp), out,
                                                  out_pitch, out_plane, flag, s);
         if (e != cudaErrorNotSupported) {
-            note_kernel("exact_row_prefix+exact_col_chain+exact_gwalk");
+            note_kernel(chains ? "exact_row_prefix+exact_col_chain+exact_gwalk"
+                               : "exact_row_carries+exact_table_strip+exact_gwalk");
             return e;
         }
     }
@@ -659,11 +968,13 @@ cudaError_t exact_select(const PlaneView& in, const Geometry& g, int radius, con
         const cudaError_t e = kTwalk[radius](in, g, sat, static_cast<size_t>(tp), out, out_pitch,
                                              out_plane, flag, s);
         if (e != cudaErrorNotSupported) {
-            note_kernel("exact_row_prefix+exact_col_chain+exact_twalk");
+            note_kernel(chains ? "exact_row_prefix+exact_col_chain+exact_twalk"
+                               : "exact_row_carries+exact_table_strip+exact_twalk");
             return e;
         }
     }
-    note_kernel("exact_row_prefix+exact_col_chain+exact_select");
+    note_kernel(chains ? "exact_row_prefix+exact_col_chain+exact_select"
+                       : "exact_row_carries+exact_table_strip+exact_select");
     switch (in.dtype) {
         case OSBF_U8:
             return launch_stencil<uint8_t>(in, g, radius, sat, out, out_pitch, out_plane, means,
@@ -693,6 +1004,15 @@ constexpr Exact2Fn kExact2[kExactFusedMaxRadius + 1] = {
 };
 static_assert(kExactFusedMaxRadius == 16, "update kExact2");
 
+// OSBF_GPU_CARRIES=warp: keep the single-warp carries kernel (A/B runs).
+bool carries_single_warp() {
+    static const bool on = [] {
+        const char* e = std::getenv("OSBF_GPU_CARRIES");
+        return e && std::strcmp(e, "warp") == 0;
+    }();
+    return on;
+}
+
 template <typename T>
 cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carries, int nsc,
                            cudaStream_t s) {
@@ -703,6 +1023,15 @@ cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carri
     if (e != cudaSuccess) return e;
     const long long rows = static_cast<long long>(g.batch) * g.height;
     const long long warps = (rows + 31) / 32;
+    if (warps <= 4 * 148 && !carries_single_warp()) {
+        // few rows: loader warps + a chain warp per 32 rows
+        static std::atomic<unsigned long long> done_pipe{0};
+        if ((e = ensure_smem(exact_row_carries_pipe<T>, RC_SMEM, done_pipe)) != cudaSuccess) return e;
+        exact_row_carries_pipe<T><<<static_cast<unsigned>(warps), 32 * (TS_LOADERS + 1), RC_SMEM, s>>>(
+            static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height, rows,
+            nsc);
+        return cudaGetLastError();
+    }
     if (warps <= 2 * 148) {  // about one warp per SM: deep single-warp CTAs
         ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>
             <<<static_cast<unsigned>(warps), 32, ex2::K1D_SMEM, s>>>(
@@ -716,6 +1045,52 @@ cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carri
     return cudaGetLastError();
 }
 }  // namespace
+
+// `carries` needs batch * height * (width / 16 + 1) doubles: it fits the
+// row-prefix workspace (batch * height * width) of exact_build_sat's contract.
+cudaError_t build_sat_strips(const PlaneView& in, const Geometry& g, double* carries, double* sat,
+                             long long tp, unsigned* flag, unsigned* reset, cudaStream_t s,
+                             LaunchCounter& lc) {
+    const int nsc = g.width / ex2::SW + 1;
+    if (reset) {  // this pass's flag starts clear (the strips may raise it)
+        if (cudaError_t e = cudaMemsetAsync(reset, 0, sizeof(unsigned), s)) return e;
+    }
+    cudaError_t e;
+    switch (in.dtype) {
+        case OSBF_U8: e = launch_carries<uint8_t>(in, g, carries, nsc, s); break;
+        case OSBF_F32: e = launch_carries<float>(in, g, carries, nsc, s); break;
+        default: e = launch_carries<double>(in, g, carries, nsc, s); break;
+    }
+    ++lc.launches;
+    if (e != cudaSuccess) return e;
+    dim3 grid((g.width + 1 + 31) / 32, g.batch);  // strips of 32 table columns
+    auto go = [&](auto tag) -> cudaError_t {
+        using T = decltype(tag);
+        static const int forced = [] {  // OSBF_GPU_TABLE_STAGES=6/16: A/B runs
+            const char* e2 = std::getenv("OSBF_GPU_TABLE_STAGES");
+            return e2 ? atoi(e2) : 0;
+        }();
+        const bool deep = forced ? forced > TS_STAGES
+                                 : static_cast<long long>(grid.x) * grid.y <= 2 * 148;
+        auto launch = [&](auto kern, size_t smem,
+                          std::atomic<unsigned long long>& done) -> cudaError_t {
+            if (cudaError_t e2 = ensure_smem(kern, smem, done)) return e2;
+            kern<<<grid, TS_THREADS, smem, s>>>(static_cast<const T*>(in.base), in.pitch, in.plane,
+                                                carries, nsc, sat, tp, g.width, g.height, flag);
+            return cudaGetLastError();
+        };
+        static std::atomic<unsigned long long> d0{0}, d1{0};
+        return deep ? launch(exact_table_strip<T, TS_STAGES_DEEP>, ts_smem(TS_STAGES_DEEP), d0)
+                    : launch(exact_table_strip<T, TS_STAGES>, ts_smem(TS_STAGES), d1);
+    };
+    switch (in.dtype) {
+        case OSBF_U8: e = go(uint8_t{}); break;
+        case OSBF_F32: e = go(float{}); break;
+        default: e = go(double{}); break;
+    }
+    ++lc.launches;
+    return e;
+}
 
 // Band height for under-occupied launches (few strips x planes): enough
 // bands for ~4 CTAs per SM, each at least 128 rows (it re-walks 2 blocks).

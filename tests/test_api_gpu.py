@@ -59,9 +59,9 @@ def test_launch_counter_counts_kernels(ctx):
     x = torch.rand((64, 64), dtype=torch.float64, device="cuda")
     before = ctx.launches
     ctx.iterate(x, 2, 3, mode="exact")
-    # a lone small plane: the whole-table path, 3 kernels per exact pass
-    # (row prefixes, column chains, stencil)
-    assert ctx.launches - before == 9 and "exact_col_chain" in ctx.last_kernel
+    # the whole-table path: 3 kernels per exact pass (row carries, strip
+    # table builder, stencil walk)
+    assert ctx.launches - before == 9 and "exact_table_strip" in ctx.last_kernel
     xb = torch.rand((300, 64, 64), dtype=torch.float64, device="cuda")
     import paper_2108_05021_b200 as ob
 
