@@ -216,14 +216,27 @@ osbf_status one_pass(osbf_ctx* ctx, const osbf_gpu::PlaneView& src, const osbf_g
     // (bit-identical to the reference, hence also within the fast mode's
     // tolerance), like the reference accepts any r.
     if (mode == OSBF_MODE_FAST && r > osbf_gpu::kFastMaxRadius) {
-        // (whole planes: the generic walk up to r = 56; past that the exact
-        // whole-table kernels measured as fast, 27 vs 30 ms per 32768^2 pass
-        // at r = 64, and their cost does not grow with r)
-        // (OSBF_GPU_FAST / osbf_gpu_set_fast_kernel "vwalk": always, for tests)
-        const bool forced = fast_family_forced("vwalk");
-        if (dst && !means && !sel && r <= osbf_gpu::fast_generic_max_radius() &&
-            (forced || (r <= osbf_gpu::kFastGenericPlaneMaxRadius &&
-                        osbf_gpu::fast_generic_fills(g, r)))) {
+        // Whole planes above the templated radii run the exact table path: it
+        // is bit-identical to the reference (so within fast mode's tolerance),
+        // its cost does not grow with r, and since the strip table builder and
+        // the generic stencil walk it is faster than the generic fast walk at
+        // every r > 16 (32768^2: 14.1 vs 14.9 ms per pass at r = 17, 14.6 vs
+        // 22.3 at r = 32; profiles/r02_exact_paths.jsonl).  The generic walk
+        // (osbf_fast_vwalk.cu) serves row bands, which the table path cannot
+        // split, a table workspace that cannot be allocated, and
+        // OSBF_GPU_FAST / osbf_gpu_set_fast_kernel "vwalk".
+        bool walk = fast_family_forced("vwalk");
+        if (!walk && dst && !means && !sel && r <= osbf_gpu::fast_generic_max_radius()) {
+            const size_t n = static_cast<size_t>(g.batch) * g.width * g.height;
+            const size_t tp = (static_cast<size_t>(g.width) + 2) & ~static_cast<size_t>(1);
+            const size_t ns = static_cast<size_t>(g.batch) * tp * (g.height + 1);
+            if (ctx->rowpfx.ensure(n * sizeof(double)) != cudaSuccess ||
+                ctx->sat.ensure((ns + 2) * sizeof(double)) != cudaSuccess) {
+                (void)cudaGetLastError();
+                walk = true;
+            }
+        }
+        if (walk && dst && !means && !sel && r <= osbf_gpu::fast_generic_max_radius()) {
             const cudaError_t e =
                 osbf_gpu::fast_generic_step(src, g, r, dst, dp, dpl, s, ctx->lc);
             if (e != cudaErrorNotSupported) {

@@ -134,8 +134,7 @@ __global__ void __launch_bounds__(NT, 4)
     if (tid == 0)
         for (int q = 0; q < ns; ++q) tma::mbar_init(&full[q], 1);
     __syncthreads();
-    auto issue = [&](int c) {  // thread 0: chunk c into stage c % ns
-        const int q = c % ns;
+    auto issue = [&](int c, int q) {  // thread 0: chunk c into stage q = c % ns
         unsigned char* s0 = sm + static_cast<size_t>(q) * st.bytes;
         const int y0 = Y0 + c * CH;
         tma::mbar_arrive_expect_tx(&full[q], st.tx);
@@ -145,7 +144,7 @@ __global__ void __launch_bounds__(NT, 4)
         tma::load_3d(s0 + st.offU, &map_u, X0, y0, b, &full[q]);
     };
     if (tid == 0)
-        for (int c = 0; c < ns && c < nchunks; ++c) issue(c);
+        for (int c = 0; c < ns && c < nchunks; ++c) issue(c, c);
 
     const bool safe = *unsafe_flag == 0u;
     const int x = min(X0 + tid, W - 1);  // lanes past the image compute column W-1, never store
@@ -168,9 +167,10 @@ __global__ void __launch_bounds__(NT, 4)
     const double y_hl = __ddiv_rn(1.0, n_hl), y_hr = __ddiv_rn(1.0, n_hr);
     const double y_v = __ddiv_rn(1.0, n_v);
 
+    int q = 0;             // stage of chunk c (c % ns, without the division)
+    unsigned phase = 0;    // (c / ns) & 1
     for (int c = 0; c < nchunks; ++c) {
-        const int q = c % ns;
-        tma::mbar_wait(&full[q], (c / ns) & 1);
+        tma::mbar_wait(&full[q], phase);
         const unsigned char* s0 = sm + static_cast<size_t>(q) * st.bytes;
         // the thread's four corner columns of the stage's first table row;
         // rows of the A / B / C boxes are immediate offsets from them
@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(NT, 4)
         __syncthreads();  // every thread is past chunk c: its stage is free
         if (tid == 0 && c + ns < nchunks) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            issue(c + ns);
+            issue(c + ns, q);
+        }
+        if (++q == ns) {
+            q = 0;
+            phase ^= 1u;
         }
     }
 }

@@ -372,17 +372,6 @@ cudaError_t fast_generic_step(const PlaneView& in, const Geometry& g, int radius
     return e;
 }
 
-bool fast_generic_fills(const Geometry& g, int radius) {
-    // under one wave of CTAs the serial block walks dominate; the exact
-    // whole-table path (parallel stencil) is then the faster fallback
-    const int sw = vwalk::strip_width(radius, 2);
-    if (!sw) return false;
-    const long long strips = (g.width + sw - 1) / sw;
-    const long long blocks =
-        (g.out_row0 + g.height - 1) / vwalk::BLOCK - g.out_row0 / vwalk::BLOCK + 1;
-    return strips * blocks * g.batch >= 148 * 4;
-}
-
 int fast_generic_max_radius() {
     // the largest radius every input dtype's staged row fits (one TMA box,
     // strip >= 32 columns, shared memory within the CTA limit)

@@ -166,13 +166,6 @@ cudaError_t fast_generic_step(const PlaneView& in, const Geometry& g, int radius
                               size_t out_pitch, size_t out_plane, cudaStream_t s,
                               LaunchCounter& lc);
 int fast_generic_max_radius();
-// Whether a whole-plane launch gives the generic walk at least one wave.
-bool fast_generic_fills(const Geometry& g, int radius);
-// Whole-plane fast passes use the generic walk up to this radius (crossover
-// with the exact whole-table path, measured); row bands use it up to
-// fast_generic_max_radius() (the exact path cannot be banded).
-constexpr int kFastGenericPlaneMaxRadius = 56;
-
 // k = 2..4 fast passes in one launch (temporal blocking, radius <= 4).
 // Returns cudaErrorNotSupported (nothing launched) when the radius / layout /
 // k has no multi-pass kernel; the caller then runs fewer passes per launch.

@@ -119,18 +119,21 @@ def test_beyond_generic_radius_runs_exact(ctx, oracle_lib):
     assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, r, 2)))
 
 
-def test_small_plane_prefers_exact_over_generic_walk(ctx, oracle_lib):
-    """A whole plane too small to give the generic walk one wave runs the
-    exact kernels (bit-identical) instead."""
+def test_whole_planes_above_16_run_the_exact_table_path(ctx, oracle_lib):
+    """Whole planes at r > 16 run the exact kernels in fast mode too: they are
+    bit-identical to the reference and, since the strip table builder and the
+    generic stencil walk, faster than the generic fast walk at every such
+    radius (the walk serves row bands and can be forced)."""
     import torch
 
-    p = np.random.default_rng(8).random((300, 260)) * 10.0
-    got = ctx.iterate(torch.from_numpy(p).cuda(), 20, 2, mode="fast").cpu().numpy()
-    assert "exact" in ctx.last_kernel
-    assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 20, 2)))
+    for shape in ((300, 260), (2048, 2048)):
+        p = np.random.default_rng(8).random(shape) * 10.0
+        got = ctx.iterate(torch.from_numpy(p).cuda(), 20, 2, mode="fast").cpu().numpy()
+        assert "exact_gwalk" in ctx.last_kernel
+        assert np.array_equal(bits(got), bits(oracle_lib.osbf(p, 20, 2, threads=8)))
 
 
-def test_large_plane_runs_generic_walk(ctx, oracle_lib):
+def test_large_plane_generic_walk_forced(ctx, oracle_lib, vwalk):
     import torch
 
     p = np.random.default_rng(9).random((8192, 8192)) * 10.0  # 64 strips x 16 blocks
