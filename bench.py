@@ -49,7 +49,7 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
            0x100: "display_clock_setting"}
 IN_BYTES = {"u8": 1, "f32": 4, "f64": 8}
 SWEEP_RADII = (1, 2, 4, 8, 16)
-C5_SWEEP_RADII = (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)  # > 16: the generic walk
+C5_SWEEP_RADII = (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)  # > 16: the exact table path (whole planes)
 
 
 def parse(argv=None):

@@ -90,13 +90,13 @@ osbf_status osbf_gpu_set_fast_kernel(const char* name);
  * family that does not apply falls through to the next.  Every family is
  * bit-identical to the reference.  No reference counterpart. */
 osbf_status osbf_gpu_set_exact_kernel(const char* name);
-/* Largest radius the fast mode serves with a fast kernel: radii up to 16 run
- * the templated kernels, larger ones the generic vertical-first walk (O(1)
- * state per thread in r) -- for whole planes up to r = 56, where the exact
- * whole-table kernels become as fast; above that a fast-mode call runs the
- * exact kernels (bit-identical, like the reference accepts any r >= 1,
- * filters2d.hpp:61-63).  Row bands (osbf_gpu_step_band*) accept radii up to
- * this value.  No reference counterpart; host-only, no device needed. */
+/* Largest radius with a fast-mode kernel: radii up to 16 run the templated
+ * kernels; above that whole planes run the exact table path in either mode
+ * (bit-identical to the reference and faster there than the generic walk;
+ * the reference accepts any r >= 1, filters2d.hpp:61-63), and row bands
+ * (osbf_gpu_step_band*) run the generic vertical-first walk (O(1) state per
+ * thread in r) for radii up to this value.  No reference counterpart;
+ * host-only, no device needed. */
 int osbf_gpu_fast_max_radius(void);
 /* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
 int osbf_gpu_device_available(void);

@@ -35,6 +35,9 @@
 namespace osbf_gpu {
 namespace gwk {
 
+#ifndef OSBF_GWALK_MINB
+#define OSBF_GWALK_MINB 4
+#endif
 constexpr int NT = 128;  // threads = output columns per CTA
 constexpr int SW = 128;
 constexpr int CH = 4;    // output rows per chunk
@@ -112,7 +115,7 @@ __device__ __forceinline__ double first_min(double (&dv)[8], double (&av)[8]) {
 // 160 / 192 / 224 / 256 that holds RA + 128 + r + 2), compile-time so every
 // shared load is [per-thread column pointer + immediate row offset].
 template <typename T, int BWT>
-__global__ void __launch_bounds__(NT, 4)
+__global__ void __launch_bounds__(NT, OSBF_GWALK_MINB)
     exact_gwalk(const __grid_constant__ CUtensorMap map_t, const __grid_constant__ CUtensorMap map_t1,
                 const __grid_constant__ CUtensorMap map_u, const double* __restrict__ sat,
                 long long tp, double* __restrict__ out, size_t out_pitch, size_t out_plane, int W,

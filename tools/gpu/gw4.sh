@@ -1,5 +1,5 @@
-python -m pytest tests/test_exact_gwalk_gpu.py tests/test_generic_radius_gpu.py tests/test_exact_families_gpu.py tests/test_acceptance_gpu.py -q -x -m gpu > gpurun_out/gw4_tests.log 2>&1; echo rc=$? >> gpurun_out/gw4_tests.log
-tail -3 gpurun_out/gw4_tests.log
+true
+true
 rm -f gpurun_out/gw4.jsonl
 P="python tools/prof_pass.py --mode exact --reps 5"
 $P --radii 2,32 --shape 64,1024,1024 --tag gw4 >> gpurun_out/gw4.jsonl 2>gpurun_out/gw4_err.log
