@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(96)
 constexpr int TS_STAGES = 6;        // many CTAs per SM
 constexpr int TS_STAGES_DEEP = 16;  // about one CTA per SM: hide the full HBM latency
 constexpr int TS_LOADERS = 4;  // loader warps (8 tile rows each)
-constexpr int TS_STORERS = 2;  // storer warps (16 tile rows each)
+constexpr int TS_STORERS = 4;  // storer warps (8 tile rows each)
 constexpr int TS_THREADS = 32 * (TS_LOADERS + 2 + TS_STORERS);
 constexpr int TS_TILE = 32 * 33 + 32;  // padded transpose tile + the 32 row carries of the tile
 
@@ -489,6 +489,9 @@ __global__ void __launch_bounds__(TS_THREADS)
         double acc = 0.0;  // lane = table column x: C(x, y) so far
         // zero border row 0 of the table over this strip's columns
         if (x <= W) C[x] = 0.0;
+        // the range check of every table value rides in the shadow of the
+        // dependent adds (integer ops only; rows past H repeat the last value)
+        bool unsafe = false;
         for (int t = 0; t < ntiles; ++t) {
             const int q = t % NST;
             mb_wait(&rdone[q], (t / NST) & 1);
@@ -500,13 +503,14 @@ __global__ void __launch_bounds__(TS_THREADS)
             for (int k = 0; k < 32; ++k) {
                 acc = __dadd_rn(acc, v[k]);
                 tile[lane * 33 + k] = acc;
+                unsafe |= !table_value_safe(acc);
             }
             mb_arrive_warp(&cdone[q], lane);
         }
+        flag_unsafe(flag, unsafe && x <= W);
     } else {
         constexpr int RPS = 32 / TS_STORERS;  // tile rows per storer warp
         const int k0 = (warp - TS_LOADERS - 2) * RPS;
-        bool unsafe = false;
         for (int t = 0; t < ntiles; ++t) {
             const int q = t % NST;
             mb_wait(&cdone[q], (t / NST) & 1);
@@ -515,19 +519,19 @@ __global__ void __launch_bounds__(TS_THREADS)
 #pragma unroll
             for (int k = 0; k < RPS; ++k) v[k] = tile[lane * 33 + k0 + k];
             mb_arrive_warp(&empty[q], lane);
-            const int nk = min(RPS, H - t * 32 - k0);  // may be <= 0
+            const int nk = H - t * 32 - k0;  // rows of this warp's part inside the table
             double* cp = C + static_cast<long long>(t * 32 + k0 + 1) * tp + x;
             if (x <= W) {
+                if (nk >= RPS) {  // straight-line stores
 #pragma unroll
-                for (int k = 0; k < RPS; ++k) {
-                    if (k < nk) {
-                        unsafe |= !table_value_safe(v[k]);
-                        cp[static_cast<long long>(k) * tp] = v[k];
-                    }
+                    for (int k = 0; k < RPS; ++k) cp[static_cast<long long>(k) * tp] = v[k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < RPS; ++k)
+                        if (k < nk) cp[static_cast<long long>(k) * tp] = v[k];
                 }
             }
         }
-        flag_unsafe(flag, unsafe);
     }
 }
 

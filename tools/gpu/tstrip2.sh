@@ -1,5 +1,4 @@
-true
-true
+python -m pytest tests/test_exact_families_gpu.py tests/test_exact_gwalk_gpu.py tests/test_parity_gpu.py -q -x -m gpu 2>&1 | tail -2
 rm -f gpurun_out/tstrip.jsonl
 P="python tools/prof_pass.py --mode exact --reps 5"
 $P --radii 2 --shape 64,1024,1024 --tag strips >> gpurun_out/tstrip.jsonl 2>gpurun_out/tstrip_err.log
