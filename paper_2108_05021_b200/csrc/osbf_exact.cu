@@ -441,20 +441,59 @@ __global__ void __launch_bounds__(TS_THREADS)
         const T* src = in + static_cast<size_t>(b) * in_plane + (u_ok ? ux : 0);
         // loader 0 also brings the tile's row carries R(x0 - 1, y), lane = row
         const double* crow = carries + static_cast<size_t>(b) * H * nsc + x0 / 16;
-        for (int t = 0; t < ntiles; ++t) {
-            const int q = t % NST;
-            if (t >= NST) mb_wait(&empty[q], ((t / NST) - 1) & 1);
-            double* tile = tring + q * TS_TILE;
-            if (warp == 0) {
-                const int y = t * 32 + lane;
-                const bool ok = y < H;
-                if constexpr (sizeof(T) == 8)
+        if constexpr (sizeof(T) == 8) {
+            for (int t = 0; t < ntiles; ++t) {
+                const int q = t % NST;
+                if (t >= NST) mb_wait(&empty[q], ((t / NST) - 1) & 1);
+                double* tile = tring + q * TS_TILE;
+                if (warp == 0) {
+                    const int y = t * 32 + lane;
+                    const bool ok = y < H;
                     cpa8(tile + 32 * 33 + lane, crow + (ok ? static_cast<size_t>(y) * nsc : 0), ok);
-                else
-                    tile[32 * 33 + lane] = ok ? crow[static_cast<size_t>(y) * nsc] : 0.0;
+                }
+                load_tile_rows<T>(tile, src + static_cast<size_t>(t) * 32 * in_pitch, in_pitch,
+                                  warp * (32 / TS_LOADERS), H - t * 32, u_ok, lane, &full[q]);
             }
-            load_tile_rows<T>(tile, src + static_cast<size_t>(t) * 32 * in_pitch, in_pitch,
-                              warp * (32 / TS_LOADERS), H - t * 32, u_ok, lane, &full[q]);
+        } else {
+            // uint8 / float32 input goes through registers: keep the loads of
+            // PF tiles in flight per warp (a register ring), convert and store
+            // a tile once its stage is free
+            constexpr int RPL = 32 / TS_LOADERS, PF = 3;
+            const int rr0 = warp * RPL;
+            T buf[PF][RPL];
+            double cbuf[PF];
+            auto fetch = [&](T (&v)[RPL], double& c, int t) {
+                const T* rs = src + static_cast<size_t>(t) * 32 * in_pitch;
+#pragma unroll
+                for (int j = 0; j < RPL; ++j) {
+                    const bool ok = u_ok && t * 32 + rr0 + j < H;
+                    v[j] = ok ? rs[static_cast<size_t>(rr0 + j) * in_pitch] : T(0);
+                }
+                const int y = t * 32 + lane;
+                c = (warp == 0 && y < H) ? crow[static_cast<size_t>(y) * nsc] : 0.0;
+            };
+            auto put = [&](const T (&v)[RPL], double c, int t) {
+                const int q = t % NST;
+                if (t >= NST) mb_wait(&empty[q], ((t / NST) - 1) & 1);
+                double* tile = tring + q * TS_TILE;
+                if (warp == 0) tile[32 * 33 + lane] = c;
+#pragma unroll
+                for (int j = 0; j < RPL; ++j) tile[lane * 33 + rr0 + j] = to_f64(v[j]);
+                mb_arrive(&full[q]);
+            };
+#pragma unroll
+            for (int i = 0; i < PF; ++i)
+                if (i < ntiles) fetch(buf[i], cbuf[i], i);
+            for (int t0 = 0; t0 < ntiles; t0 += PF) {
+#pragma unroll
+                for (int i = 0; i < PF; ++i) {
+                    const int t = t0 + i;
+                    if (t < ntiles) {
+                        put(buf[i], cbuf[i], t);
+                        if (t + PF < ntiles) fetch(buf[i], cbuf[i], t + PF);
+                    }
+                }
+            }
         }
     } else if (warp == TS_LOADERS) {
         // lane = row of the tile: column 0 is the carry R(x0 - 1, y), then the chain
@@ -571,12 +610,12 @@ __global__ void __launch_bounds__(32 * (TS_LOADERS + 1))
                 base[j] = b * static_cast<long long>(plane) + y * static_cast<long long>(pitch);
             }
         }
-        for (int c = 0; c < nchunks; ++c) {
-            const int q = c % RC_STAGES;
-            if (c >= RC_STAGES) mb_wait(&empty[q], ((c / RC_STAGES) - 1) & 1);
-            double* t = cring + q * 32 * 33;
-            const int x = 32 * c + lane;
-            if constexpr (sizeof(T) == 8) {
+        if constexpr (sizeof(T) == 8) {
+            for (int c = 0; c < nchunks; ++c) {
+                const int q = c % RC_STAGES;
+                if (c >= RC_STAGES) mb_wait(&empty[q], ((c / RC_STAGES) - 1) & 1);
+                double* t = cring + q * 32 * 33;
+                const int x = 32 * c + lane;
 #pragma unroll
                 for (int j = 0; j < RPL; ++j) {
                     const bool ok = base[j] >= 0 && x < W;
@@ -584,14 +623,37 @@ __global__ void __launch_bounds__(32 * (TS_LOADERS + 1))
                          reinterpret_cast<const double*>(in) + (ok ? base[j] + x : 0), ok);
                 }
                 mb_arrive_cpasync(&full[q]);
-            } else {
-                T v[RPL];
+            }
+        } else {
+            // through registers: the loads of PF chunks stay in flight per warp
+            constexpr int PF = 3;
+            T buf[PF][RPL];
+            auto fetch = [&](T (&v)[RPL], int c) {
+                const int x = 32 * c + lane;
 #pragma unroll
                 for (int j = 0; j < RPL; ++j)
                     v[j] = (base[j] >= 0 && x < W) ? in[base[j] + x] : T(0);
+            };
+            auto put = [&](const T (&v)[RPL], int c) {
+                const int q = c % RC_STAGES;
+                if (c >= RC_STAGES) mb_wait(&empty[q], ((c / RC_STAGES) - 1) & 1);
+                double* t = cring + q * 32 * 33;
 #pragma unroll
                 for (int j = 0; j < RPL; ++j) t[lane * 33 + warp * RPL + j] = to_f64(v[j]);
                 mb_arrive(&full[q]);
+            };
+#pragma unroll
+            for (int i = 0; i < PF; ++i)
+                if (i < nchunks) fetch(buf[i], i);
+            for (int c0 = 0; c0 < nchunks; c0 += PF) {
+#pragma unroll
+                for (int i = 0; i < PF; ++i) {
+                    const int c = c0 + i;
+                    if (c < nchunks) {
+                        put(buf[i], c);
+                        if (c + PF < nchunks) fetch(buf[i], c + PF);
+                    }
+                }
             }
         }
     } else {
@@ -864,6 +926,11 @@ cudaError_t build_sat_strips(const PlaneView& in, const Geometry& g, double* car
 
 bool table_deep(const Geometry& g);
 bool table_uses_strips(const PlaneView& in, const Geometry& g) {
+    static const bool strips_forced = [] {  // OSBF_GPU_TABLE=strips: always (A/B runs)
+        const char* e = std::getenv("OSBF_GPU_TABLE");
+        return e && std::strcmp(e, "strips") == 0;
+    }();
+    if (strips_forced) return true;
     return !table_chains_forced() && !(in.dtype == OSBF_F32 && !table_deep(g));
 }
 
