@@ -578,10 +578,11 @@ __global__ void __launch_bounds__(TS_THREADS)
 // or fewer): CTA per 32 rows as loader warps + one chain warp over a ring of
 // 32 x 32 chunks, so the serial chain (row += src[x], integral.hpp:25) is not
 // slowed by the copy instructions.  Same values as ex2::exact_row_carries.
-constexpr int RC_STAGES = 16;
-constexpr size_t RC_SMEM = sizeof(double) * RC_STAGES * 32 * 33;
+constexpr int RC_STAGES_DEEP = 16;  // about one CTA per SM
+constexpr int RC_STAGES_MANY = 4;   // several CTAs per SM
+constexpr size_t rc_smem(int stages) { return sizeof(double) * stages * 32 * 33; }
 
-template <typename T>
+template <typename T, int RC_STAGES>
 __global__ void __launch_bounds__(32 * (TS_LOADERS + 1))
     exact_row_carries_pipe(const T* __restrict__ in, size_t pitch, size_t plane,
                            double* __restrict__ carries, int W, int H, long long rows, int nsc) {
@@ -925,14 +926,7 @@ cudaError_t build_sat_strips(const PlaneView& in, const Geometry& g, double* car
                              LaunchCounter& lc);
 
 bool table_deep(const Geometry& g);
-bool table_uses_strips(const PlaneView& in, const Geometry& g) {
-    static const bool strips_forced = [] {  // OSBF_GPU_TABLE=strips: always (A/B runs)
-        const char* e = std::getenv("OSBF_GPU_TABLE");
-        return e && std::strcmp(e, "strips") == 0;
-    }();
-    if (strips_forced) return true;
-    return !table_chains_forced() && !(in.dtype == OSBF_F32 && !table_deep(g));
-}
+bool table_uses_strips(const PlaneView&, const Geometry&) { return !table_chains_forced(); }
 
 bool table_deep(const Geometry& g) {
     static const int forced = [] {  // OSBF_GPU_TABLE_DEEP=0/1: A/B runs
@@ -956,9 +950,8 @@ cudaError_t exact_build_sat(const PlaneView& in, const Geometry& g, double* rowp
     unsigned* const reset = table_flag;
     unsigned* const flag = table_flag ? table_flag : table_flag_address();
     if (!flag) return cudaErrorInvalidDevicePointer;
-    // float32 input (a first pass) with many rows: the strip builder's
-    // register-staged loads lose to the plain chain kernels (256 x 1024^2:
-    // 4.5-5.5 vs 3.7 ms); every other case builds by strips
+    // every dtype and shape builds by strips (float32 256 x 1024^2: 3.23 vs
+    // 3.65 ms with the chain kernels, uint8 64 x 1024^2: 0.82 vs 1.65)
     if (table_uses_strips(in, g)) return build_sat_strips(in, g, rowpfx, sat, tp, flag, reset, s, lc);
     if (table_deep(g)) {
         switch (in.dtype) {
@@ -1094,14 +1087,26 @@ cudaError_t launch_carries(const PlaneView& in, const Geometry& g, double* carri
     if (e != cudaSuccess) return e;
     const long long rows = static_cast<long long>(g.batch) * g.height;
     const long long warps = (rows + 31) / 32;
-    if (warps <= 4 * 148 && !carries_single_warp()) {
-        // few rows: loader warps + a chain warp per 32 rows
-        static std::atomic<unsigned long long> done_pipe{0};
-        if ((e = ensure_smem(exact_row_carries_pipe<T>, RC_SMEM, done_pipe)) != cudaSuccess) return e;
-        exact_row_carries_pipe<T><<<static_cast<unsigned>(warps), 32 * (TS_LOADERS + 1), RC_SMEM, s>>>(
-            static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height, rows,
-            nsc);
-        return cudaGetLastError();
+    if (!carries_single_warp()) {
+        // loader warps + a chain warp per 32 rows; a deep ring when there is
+        // about one CTA per SM
+        static std::atomic<unsigned long long> done_deep{0}, done_many{0};
+        auto launch = [&](auto kern, int stages,
+                          std::atomic<unsigned long long>& done) -> cudaError_t {
+            if (cudaError_t e2 = ensure_smem(kern, rc_smem(stages), done)) return e2;
+            kern<<<static_cast<unsigned>(warps), 32 * (TS_LOADERS + 1), rc_smem(stages), s>>>(
+                static_cast<const T*>(in.base), in.pitch, in.plane, carries, g.width, g.height,
+                rows, nsc);
+            return cudaGetLastError();
+        };
+        static const bool many_ok = [] {  // OSBF_GPU_CARRIES=old: the 2-warp kernel for many rows
+            const char* e2 = std::getenv("OSBF_GPU_CARRIES");
+            return !(e2 && std::strcmp(e2, "old") == 0);
+        }();
+        if (warps <= 4 * 148)
+            return launch(exact_row_carries_pipe<T, RC_STAGES_DEEP>, RC_STAGES_DEEP, done_deep);
+        if (many_ok)
+            return launch(exact_row_carries_pipe<T, RC_STAGES_MANY>, RC_STAGES_MANY, done_many);
     }
     if (warps <= 2 * 148) {  // about one warp per SM: deep single-warp CTAs
         ex2::exact_row_carries<T, 1, ex2::K1D_STAGES>
