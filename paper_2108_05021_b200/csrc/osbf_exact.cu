@@ -807,12 +807,16 @@ __device__ __forceinline__ void stencil_px(const T* __restrict__ in, size_t in_p
 
 // The shared sticky flag word (callers that pass no flag of their own).
 unsigned* table_flag_address() {
-    static unsigned* flag = [] {
-        void* p = nullptr;
-        return cudaGetSymbolAddress(&p, g_table_unsafe) == cudaSuccess ? static_cast<unsigned*>(p)
-                                                                       : nullptr;
-    }();
-    return flag;
+    // the symbol lives on every device: one address per device ordinal
+    static std::atomic<unsigned*> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::atomic<unsigned*>& slot = cache[dev & 63];
+    if (unsigned* p = slot.load(std::memory_order_acquire)) return p;
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_table_unsafe) != cudaSuccess) return nullptr;
+    slot.store(static_cast<unsigned*>(p), std::memory_order_release);
+    return static_cast<unsigned*>(p);
 }
 
 constexpr int kStencilRows = 4;  // rows per thread (block: 32 x 8 threads, 32 x 32 pixels)

@@ -78,6 +78,24 @@ def test_null_context_is_invalid_argument():
     assert lib.osbf_gpu_last_error() == b"null context"
 
 
+def test_kernel_family_overrides_validate_names():
+    """The diagnostic family switches are host-side state: known names (and
+    None / "" to clear) are accepted without a device, unknown ones rejected."""
+    import paper_2108_05021_b200 as ob
+
+    lib = ob.lib()
+    try:
+        for fam in ("strip", "gwalk", "twalk", "stencil"):
+            assert lib.osbf_gpu_set_exact_kernel(fam.encode()) == 0
+        assert lib.osbf_gpu_set_exact_kernel(b"no-such-family") != 0
+        assert b"unknown exact kernel family" in lib.osbf_gpu_last_error()
+        assert lib.osbf_gpu_set_fast_kernel(b"walk") == 0
+        assert lib.osbf_gpu_set_fast_kernel(b"no-such-family") != 0
+    finally:
+        assert lib.osbf_gpu_set_exact_kernel(None) == 0
+        assert lib.osbf_gpu_set_fast_kernel(b"") == 0
+
+
 def test_python_value_types_mirror_reference():
     import paper_2108_05021_b200 as ob
 
