@@ -288,10 +288,16 @@ cudaError_t exact_gwalk_launch_class(const PlaneView& in, const Geometry& g, int
     const int strips = (g.width + SW - 1) / SW;
     // row blocks: 256 rows, fewer when that leaves the device under two
     // waves of 4 CTAs per SM
+    static const int kBh = [] {
+        const char* e = std::getenv("OSBF_GPU_GWALK_BH");  // diagnostic override
+        const int v = e ? atoi(e) : 0;
+        return v >= 16 ? v : 0;
+    }();
     int bh = 256;
     while (bh > 64 && static_cast<long long>(strips) * ((g.height + bh - 1) / bh) * g.batch <
                           2LL * 148 * 4)
         bh /= 2;
+    if (kBh) bh = kBh;
     dim3 grid(strips, (g.height + bh - 1) / bh, g.batch);
     exact_gwalk<T, BWT><<<grid, NT, smem, s>>>(mt, mt1, mu, sat, static_cast<long long>(tpitch),
                                                out, op, opl, g.width, g.height, bh, r, kNs,
